@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Headline benchmark: Nekbone Ax (FP64) at E=4096, p=9 on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one application of the local operator w = A_local u over all
+E=4096 elements of degree p=9 (n=10) with a random metric (BASELINE.json
+config 2, north_star).  Inputs are resident in HBM; the per-step working set
+(u + g + w = 262 MB) exceeds the 126 MB L2 and two input sets are rotated,
+so every step streams from HBM.  Prints ONE JSON line (rank 0).
+
+Multi-GPU (torchrun, one rank per GPU): Ax is element-local, so each rank
+applies the operator to its own E=4096 elements (weak scaling, no
+data-path collective); value = all ranks' flops / max-over-ranks time.
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port in oracle/, OpenMP over all host cores) on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+E_HEAD, N_HEAD = 4096, 10
+METRIC = "Ax FP64 GFLOP/s at E=4096,p=9 (1/2/4/8 GPU) and % of B200 HBM roofline"
+UNIT = "GFLOP/s"
+
+
+def ax_flops(E, n):
+    return E * n ** 3 * (12 * n + 15)  # sembench/kernels.py:121-125
+
+
+def ax_bytes(E, n):
+    return E * n ** 3 * 64  # u 8 + g 48 + w 8 bytes per point
+
+
+# --------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks / throttle reasons during a region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in self.rows if num(r[0]) is not None]
+        mx = [num(r[1]) for r in self.rows if num(r[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[4 + i].lower().startswith("active")})
+        # median over the busiest half of the samples (the region is short)
+        busy = sorted(sm)[len(sm) // 2:] if sm else []
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows),
+                "power_w_max": max((num(r[2]) or 0.0) for r in self.rows)}
+
+
+# ------------------------------------------------------------- CPU side ----
+def cpu_ax_sample(budget_s: float, reps_min: int = 3):
+    """Oracle port (C, OpenMP) timed on a bounded sample of the workload."""
+    import oracle as O
+    from paper_2005_13425_b200.basis import build_basis
+    b = build_basis(N_HEAD)
+    E = E_HEAD
+    u = O.random_field(E, N_HEAD, 1)
+    g = O.random_field(6 * E, N_HEAD, 2).reshape(E, 6, N_HEAD, N_HEAD, N_HEAD)
+    threads = O.max_threads()
+    t0 = time.perf_counter()
+    O.ax_layered(u, g, b.diff, b.diff_t, threads)  # warm-up (page-in, thread pool)
+    t_one = time.perf_counter() - t0
+    times = []
+    start = time.perf_counter()
+    while len(times) < reps_min or (time.perf_counter() - start) < budget_s:
+        t0 = time.perf_counter()
+        O.ax_layered(u, g, b.diff, b.diff_t, threads)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 1000:
+            break
+    t = statistics.median(times)
+    return {"value": ax_flops(E, N_HEAD) / t / 1e9, "unit": UNIT, "cores": threads,
+            "kind": "port",
+            "sample": f"full E={E}, p=9 apply x {len(times)} reps (median), "
+                      f"oracle/sem_oracle.c OpenMP {threads} threads, cpu={_cpu_model()}",
+            "ms_per_apply": t * 1e3, "first_call_ms": t_one * 1e3}
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------ reference ----
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import oracle as O
+    from paper_2005_13425_b200.basis import build_basis
+    b = build_basis(N_HEAD)
+    E = E_HEAD
+    u = O.random_field(E, N_HEAD, 1)
+    g = O.random_field(6 * E, N_HEAD, 2).reshape(E, 6, N_HEAD, N_HEAD, N_HEAD)
+    threads = O.max_threads()
+    t0 = time.perf_counter()
+    O.ax_layered(u, g, b.diff, b.diff_t, threads)
+    t_full = time.perf_counter() - t0
+    # bound the whole run to ~90 s: shrink the per-step element sample if needed
+    budget = 90.0
+    frac = min(1.0, budget / max(1e-9, (args.steps + args.warmup) * t_full))
+    Es = max(1, int(E * frac))
+    us, gs = np.ascontiguousarray(u[:Es]), np.ascontiguousarray(g[:Es])
+    for _ in range(args.warmup):
+        O.ax_layered(us, gs, b.diff, b.diff_t, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.ax_layered(us, gs, b.diff, b.diff_t, threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = ax_flops(Es, N_HEAD) / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64 u and random metric g, sembench/fields.py)",
+        "config": {"workload": f"Ax layered, E={E}, p=9 (n=10), FP64, random gxyz",
+                   "elements_per_step": Es},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{Es} of {E} elements per step, oracle/sem_oracle.c "
+                                   f"(restatement of sembench/kernels.py:267-329), "
+                                   f"cpu={_cpu_model()}"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ ours ----
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2005_13425_b200 as sb
+    from paper_2005_13425_b200 import _device as dv
+    from paper_2005_13425_b200.kernels import apply_ax_into
+    from paper_2005_13425_b200.perf import measured_peaks
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n, E = N_HEAD, E_HEAD
+    basis = sb.build_basis(n)
+    sets = []
+    for s in range(2):  # two resident input sets, 2 x 262 MB > 4 x L2
+        u = sb.random_field(E, n, 1 + 10 * s + 1000 * rank, device=dev)
+        g = sb.random_field(6 * E, n, 2 + 10 * s + 1000 * rank, device=dev)
+        g = g.reshape(E, 6, n, n, n)
+        sets.append((u, g, torch.empty_like(u)))
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        u, g, w = sets[i % 2]
+        apply_ax_into(u, g, basis, w, args.variant)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize(dev)
+
+    # parity spot check of this exact configuration before timing (cheap)
+    with ClockSampler(local_rank) as clocks:
+        # soak so the clock sampler sees the sustained state of this kernel
+        t_soak = time.perf_counter()
+        i = 0
+        while time.perf_counter() - t_soak < args.soak:
+            for _ in range(200):
+                step(i)
+                i += 1
+            torch.cuda.synchronize(dev)
+        barrier()
+        torch.cuda.synchronize(dev)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    ms_step = ms_total / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    flops = ax_flops(E, n)
+    value = world * flops / (ms_step * 1e-3) / 1e9
+    peaks = measured_peaks(ROOT)
+    hbm = float(peaks["hbm_gbs"])
+    achieved_gbs = ax_bytes(E, n) / (ms_step * 1e-3) / 1e9
+
+    # ---- e2e: the public API with host buffers (pinned u in, host w out) ----
+    geom = sb.GeomFactors(values=sets[0][1])
+    u_host = sets[0][0].cpu().pin_memory()
+    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    for _ in range(2):
+        sb.apply_ax(u_host, geom, basis)
+    torch.cuda.synchronize(dev)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        w_host = sb.apply_ax(u_host, geom, basis)
+    torch.cuda.synchronize(dev)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    assert w_host.device.type == "cpu"
+    e2e_val = world * flops / e2e_s / 1e9
+
+    # ---- secondary: full Nekbone CG, 100 iterations (BASELINE config 4) ----
+    cg = None
+    if args.cg:
+        cg = bench_cg(sb, dev, 100)
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ax_ncu_summary.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_ax_sample(args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64 u and random metric g, generated on device)",
+            "config": {"workload": f"Ax layered (sem_ax), E={E} per GPU, p=9 (n=10), FP64, "
+                                   "random gxyz", "elements_per_gpu": E, "n": n,
+                       "l2": "inputs larger than L2: 2 rotating sets of 262 MB",
+                       "parallelism": f"dp{world} (element partition, no collective)"},
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved_gbs / hbm, "traffic": traffic,
+                         "peak_source": peaks.get("source"),
+                         "algorithmic_bytes_per_launch": ax_bytes(E, n),
+                         "gflops_per_gpu": flops / (ms_step * 1e-3) / 1e9,
+                         "gflops_roofline": hbm * (12 * n + 15) / 64.0},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * E * n ** 3,
+                    "d2h_bytes_per_step": 8 * E * n ** 3,
+                    "path": "apply_ax(pinned CPU tensor u, geom resident) -> CPU tensor w",
+                    "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": args.steps,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        if cg is not None:
+            line["cg_e4096_p9"] = cg
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_cg(sb, dev, iters):
+    import torch
+    from paper_2005_13425_b200 import perf
+    n, E = N_HEAD, E_HEAD
+    b = sb.build_basis(n)
+    mesh = sb.build_mesh(*sb.factor_elements(E), n, 1.0)
+    topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b, device=dev)
+    f = sb.make_rhs(E, n, topo, sb.mix64(1, E), device=dev)
+    op = sb.GlobalOperator(geom, b, topo)
+    ws = sb.CgWorkspace(topo, iters, dev)
+    sb.cg_solve(f, op, topo, sb.CgConfig(3, 0.0), workspace=ws)  # warm-up
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = sb.cg_solve(f, op, topo, sb.CgConfig(iters, 0.0), workspace=ws)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    dofs = topo.dofs
+    per_it = ms / iters
+    model_flops = perf.model_flops_per_iteration(dofs, n)
+    hbm = float(perf.measured_peaks(ROOT)["hbm_gbs"]) * 1e9
+    gf = model_flops / (per_it * 1e-3)
+    return {"iterations": res.iterations_run, "ms_per_iteration": per_it,
+            "model_gflops": gf / 1e9,
+            "paper_roofline_frac": gf / perf.roofline_peak(hbm, n),
+            "final_residual": float(res.residual_history[-1]),
+            "note": "paper Eq.(1)/(2) model: D(12n+34) flop, 240 D bytes per iteration; "
+                    "timed with CUDA events incl. one host sync at the end"}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--soak", type=float, default=1.5, help="seconds of load before timing")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cg", type=int, default=1)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

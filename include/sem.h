@@ -1,0 +1,139 @@
+/*
+ * libsem -- B200-native (sm_100a) hot path of the Nekbone / sembench
+ * spectral-element Poisson solve (arXiv 2005.13425): the local tensor-product
+ * operator Ax, the direct-stiffness summation dssum + Dirichlet mask, and the
+ * CG vector kernels (add2s1 / add2s2 / glsc3).
+ *
+ * Plain C ABI: device pointers are raw CUDA device addresses (a torch
+ * tensor's data_ptr(), a cudaMalloc result, ...), sizes are int64, and every
+ * call is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ * stream) without synchronising the host.  Every entry point returns 0 on
+ * success, otherwise a nonzero code with a message in sem_last_error().
+ * No entry point allocates device memory; scratch is caller-provided.
+ *
+ * Reference interface each entry point replaces (the reference is the
+ * Python/numba package `sembench`, paths relative to
+ * /root/reference/pkg/src/sembench/):
+ *
+ *   sem_ax             kernels.py:413-468 apply_ax (LAYERED, :267-410)
+ *   sem_dssum_box      assembly.py:113-120 dssum  (bincount order, bit-exact)
+ *   sem_mask_box       assembly.py:123-129 mask
+ *   sem_apply_global   assembly.py:132-155 apply_global
+ *   sem_add2s1         cg.py:101-104 _scale_add   p = beta*p + z
+ *   sem_add2s2         cg.py:95-98   _axpy_into   x += alpha*y
+ *   sem_glsc3*         cg.py:77-92,107-111 _wdot3 / weighted_dot
+ *   sem_cg_*           cg.py:114-193 cg_solve loop (device-resident scalars)
+ *   sem_random_field   fields.py:42-54 random_field (bit-exact SplitMix64)
+ *   sem_box_geom       mesh.py:72-91 build_geom (bit-exact)
+ */
+#ifndef SEM_H_
+#define SEM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SEM_ABI_VERSION 1
+
+/* Error codes besides cudaError_t values. */
+#define SEM_E_INVALID 1001  /* bad argument (shape, n range, null pointer) */
+#define SEM_E_BREAKDOWN 1002
+
+typedef void *sem_stream_t; /* cudaStream_t */
+
+int sem_abi_version(void);
+const char *sem_last_error(void);
+
+/* Supported points per dimension n (sembench/basis.py:17-18: 2..16). */
+int sem_min_points(void);
+int sem_max_points(void);
+
+/* ---------------------------------------------------------------- Ax ---- */
+/* w[e] = A_local u[e] for every element (kernels.py:413-468).
+ * u, w : [E][n][n][n] float64 device, i fastest; g : [E][6][n][n][n] float64
+ * device (metric g1..g6 per point, mesh.py:40-57); dx, dxt : [n][n] float64
+ * HOST arrays (basis.diff / basis.diff_t, 2 KB at most) -- they travel in the
+ * kernel's constant parameter space.  u and w must not alias. */
+int sem_ax(const double *u, const double *g, const double *dx, const double *dxt,
+           double *w, int64_t num_elements, int32_t n, sem_stream_t stream);
+
+/* Kernel-variant hook for benchmarks/ablation: variant 0 = default layered
+ * kernel; other values select alternative tilings. */
+int sem_ax_variant(const double *u, const double *g, const double *dx,
+                   const double *dxt, double *w, int64_t num_elements, int32_t n,
+                   int32_t variant, sem_stream_t stream);
+int sem_ax_num_variants(int32_t n);
+
+/* ------------------------------------------------- assembly (box mesh) -- */
+/* Element numbering e = ix + ex*(iy + ey*iz) and lattice ids of
+ * assembly.py:69-110.  `out` may equal neither `f` (out-of-place).
+ * apply_mask != 0 multiplies the summed value by the Dirichlet 0/1 mask
+ * (i.e. returns mask(dssum(f))). */
+int sem_dssum_box(const double *f, double *out, int32_t ex, int32_t ey, int32_t ez,
+                  int32_t n, int32_t apply_mask, sem_stream_t stream);
+int sem_mask_box(const double *f, double *out, int32_t ex, int32_t ey, int32_t ez,
+                 int32_t n, sem_stream_t stream);
+/* mask(dssum(A_local(mask(u)))) with `scratch` an E*n^3 float64 buffer. */
+int sem_apply_global(const double *u, const double *g, const double *dx,
+                     const double *dxt, double *w, double *scratch, int32_t ex,
+                     int32_t ey, int32_t ez, int32_t n, sem_stream_t stream);
+
+/* ------------------------------------------------------ CG vector ops -- */
+/* Bit-exact unfused updates (multiply rounded, then add rounded). */
+int sem_add2s1(double *p, const double *z, double beta, int64_t m, sem_stream_t stream);
+int sem_add2s2(double *x, const double *y, double alpha, int64_t m, sem_stream_t stream);
+
+/* Deterministic weighted dot sum_i a_i*b_i*wt_i.  The result lands in
+ * out_dev[0] (device).  `scratch` must hold sem_reduce_scratch_bytes(). */
+int64_t sem_reduce_scratch_bytes(void);
+int sem_glsc3(const double *a, const double *b, const double *wt, int64_t m,
+              double *out_dev, void *scratch, sem_stream_t stream);
+/* Same with wt = 1/multiplicity computed from the box lattice (no weight
+ * array is read). */
+int sem_glsc3_box(const double *a, const double *b, int32_t ex, int32_t ey,
+                  int32_t ez, int32_t n, double *out_dev, void *scratch,
+                  sem_stream_t stream);
+
+/* --------------------------------------------------------- CG driver ---- */
+/* Device-resident CG state (cg.py:139-186).  Layout shared with the host. */
+typedef struct sem_cg_state {
+    double rtz;        /* <r,r>_c of the current residual            */
+    double rtz_old;
+    double pap;
+    double alpha;
+    double beta;
+    double tolerance;
+    int32_t it;        /* iterations started so far                   */
+    int32_t max_iterations;
+    int32_t iterations_run;
+    int32_t stop;      /* 0 running, 1 exact zero residual (cg.py:151),
+                          2 breakdown <p,Ap> <= 0, 3 tolerance reached */
+    int32_t breakdown_it;
+    int32_t pad_;
+} sem_cg_state;
+
+/* Initialise: r = mask(f), x = p = 0, rtz = <r,r>_c, state fields. */
+int sem_cg_init(const double *f, double *x, double *r, double *p, sem_cg_state *state,
+                double *history, int32_t max_iterations, double tolerance,
+                int32_t ex, int32_t ey, int32_t ez, int32_t n, void *scratch,
+                sem_stream_t stream);
+/* Enqueue `iterations` fused CG iterations on the box operator (single GPU).
+ * w is a 2*E*n^3 scratch buffer; history receives sqrt(<r,r>_c) per iteration. */
+int sem_cg_run(const double *g, const double *dx, const double *dxt, double *x,
+               double *r, double *p, double *w, sem_cg_state *state, double *history,
+               int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+               void *scratch, sem_stream_t stream);
+
+/* ------------------------------------------------------ input builders -- */
+int sem_random_field(double *out, int64_t count, uint64_t seed, sem_stream_t stream);
+/* g for the affine box map: g1=g4=g6=(w_k*w_j)*w_i*(h/2), g2=g3=g5=0;
+ * weights is a HOST array of n GLL weights. */
+int sem_box_geom(double *g, int64_t num_elements, int32_t n, const double *weights,
+                 double extent, sem_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEM_H_ */

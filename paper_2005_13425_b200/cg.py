@@ -1,0 +1,235 @@
+"""Unpreconditioned CG with multiplicity-weighted inner products on the B200
+(contract of sembench/cg.py:53-193).
+
+Two execution paths share the reference recurrence:
+
+* **fused** -- when ``operator`` is a :class:`GlobalOperator` (the box
+  apply_global), the whole solve runs as device-resident launches
+  (``sem_cg_init`` + ``sem_cg_run``, csrc/cg.cu): alpha/beta never leave the
+  GPU, reductions are deterministic, early exits are device flags.  The host
+  synchronises once at the end (or once per iteration if a callback is set).
+* **generic** -- any other callable: each iteration calls ``operator(p)`` on
+  a CUDA tensor and uses the same sm_100a vector kernels (add2s1, add2s2,
+  glsc3).
+
+Errors follow the reference: ``CgBreakdownError`` when <p,Ap>_c <= 0, and
+``ValueError`` for a bad configuration.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from ._lib import check, load, sem_cg_state
+from .assembly import GlobalOperator, Topology, _mask_dev
+from .fields import validate_field
+from .kernels import TrafficCounters
+
+__all__ = ["CgConfig", "CgResult", "CgBreakdownError", "weighted_dot", "cg_solve",
+           "CG_VECTOR_FLOPS_PER_POINT", "CgWorkspace"]
+
+CG_VECTOR_FLOPS_PER_POINT = 12
+
+
+class CgBreakdownError(RuntimeError):
+    """<p, A p>_c was non-positive: the operator is not SPD on this subspace."""
+
+
+@dataclass
+class CgConfig:
+    max_iterations: int = 100
+    tolerance: float = 0.0
+
+    def __post_init__(self):
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be at least 1")
+        if self.tolerance < 0.0:
+            raise ValueError("tolerance must be non-negative")
+
+
+@dataclass
+class CgResult:
+    solution: object
+    residual_history: np.ndarray
+    iterations_run: int
+    counters: TrafficCounters = field(default_factory=TrafficCounters)
+
+
+def _glsc3_box_dev(a: torch.Tensor, b: torch.Tensor, topo: Topology,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
+    dev = a.device
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=dev)
+    check(load().sem_glsc3_box(dv.ptr(a), dv.ptr(b), topo.ex, topo.ey, topo.ez, topo.n,
+                               dv.ptr(out), dv.ptr(dv.reduce_scratch(dev)),
+                               dv.stream_handle(dev)), "weighted_dot")
+    return out
+
+
+def weighted_dot(u, v, topo: Topology) -> float:
+    """sum(u * v / multiplicity) -- deterministic device reduction."""
+    validate_field(u, topo.num_elements, topo.n, "u")
+    validate_field(v, topo.num_elements, topo.n, "v")
+    dev = u.device if dv.is_tensor(u) else (v.device if dv.is_tensor(v) else None)
+    ud = dv.as_device_f64(u, dev, "u")
+    vd = dv.as_device_f64(v, ud.device, "v")
+    with torch.cuda.device(ud.device):
+        out = _glsc3_box_dev(ud, vd, topo)
+        return float(out.item())
+
+
+class CgWorkspace:
+    """Device vectors and state of one fused solve (reusable across solves)."""
+
+    def __init__(self, topo: Topology, max_iterations: int, device: torch.device):
+        shape = (topo.num_elements, topo.n, topo.n, topo.n)
+        mk = lambda: torch.empty(shape, dtype=torch.float64, device=device)  # noqa: E731
+        self.x, self.r, self.p = mk(), mk(), mk()
+        self.w = torch.empty((2,) + shape, dtype=torch.float64, device=device)
+        self.history = torch.zeros(max(1, max_iterations), dtype=torch.float64, device=device)
+        self.state = torch.zeros(ctypes_sizeof_state(), dtype=torch.uint8, device=device)
+        self.scratch = torch.zeros(int(load().sem_reduce_scratch_bytes()), dtype=torch.uint8,
+                                   device=device)
+        self.device = device
+        self.max_iterations = max_iterations
+
+    def read_state(self) -> sem_cg_state:
+        raw = self.state.cpu().numpy().tobytes()
+        return sem_cg_state.from_buffer_copy(raw)
+
+
+def ctypes_sizeof_state() -> int:
+    import ctypes
+    return ctypes.sizeof(sem_cg_state)
+
+
+def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: CgConfig,
+                 callback, host: bool, ws: CgWorkspace | None = None):
+    lib = load()
+    dev = f_dev.device
+    if ws is None or ws.max_iterations < cfg.max_iterations or ws.device != dev:
+        ws = CgWorkspace(topo, cfg.max_iterations, dev)
+    s = dv.stream_handle(dev)
+    g = op.geom.device_values(dev)
+    dx = np.ascontiguousarray(op.basis.diff, dtype=np.float64)
+    dxt = np.ascontiguousarray(op.basis.diff_t, dtype=np.float64)
+    box = (topo.ex, topo.ey, topo.ez, topo.n)
+    check(lib.sem_cg_init(dv.ptr(f_dev), dv.ptr(ws.x), dv.ptr(ws.r), dv.ptr(ws.p),
+                          dv.ptr(ws.state), dv.ptr(ws.history), cfg.max_iterations,
+                          float(cfg.tolerance), *box, dv.ptr(ws.scratch), s), "cg_solve init")
+
+    def run(k: int):
+        check(lib.sem_cg_run(dv.ptr(g), dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt), dv.ptr(ws.x),
+                             dv.ptr(ws.r), dv.ptr(ws.p), dv.ptr(ws.w), dv.ptr(ws.state),
+                             dv.ptr(ws.history), k, *box, dv.ptr(ws.scratch), s), "cg_solve run")
+
+    if callback is None:
+        run(cfg.max_iterations)
+        st = ws.read_state()
+    else:
+        st = None
+        for it in range(1, cfg.max_iterations + 1):
+            run(1)
+            st = ws.read_state()
+            if st.iterations_run >= it and st.stop != 2:
+                x = dv.to_numpy(ws.x) if host else ws.x
+                r = dv.to_numpy(ws.r) if host else ws.r
+                callback(it, x, r)
+            if st.stop:
+                break
+    if st.stop == 2:
+        ppc = float(_glsc3_box_dev(ws.p, ws.p, topo).item())
+        raise CgBreakdownError(
+            f"<p, A p>_c = {st.pap:.3e} at iteration {st.breakdown_it} "
+            f"(scale <p, p>_c = {ppc:.3e}); operator is not SPD here")
+    iters = int(st.iterations_run)
+    history = dv.to_numpy(ws.history[:iters]).copy()
+    zero_exit = st.stop == 1
+    solution = ws.x.clone()
+    return solution, history, iters, zero_exit
+
+
+def _generic_solve(f_dev: torch.Tensor, operator, topo: Topology, cfg: CgConfig, counters,
+                   callback, host: bool):
+    lib = load()
+    dev = f_dev.device
+    s = dv.stream_handle(dev)
+    m = f_dev.numel()
+    r = _mask_dev(f_dev, topo)
+    x = torch.zeros_like(r)
+    p = torch.zeros_like(r)
+    dofs = topo.dofs
+    history: list[float] = []
+    rtz, iters, zero_exit = 1.0, 0, False
+
+    def dot(a, b) -> float:
+        return float(_glsc3_box_dev(a, b, topo).item())
+
+    for it in range(1, cfg.max_iterations + 1):
+        rtz_old = rtz
+        rtz = dot(r, r)
+        if rtz == 0.0:
+            iters = it
+            history.append(0.0)
+            zero_exit = True
+            if callback is not None:
+                callback(it, dv.to_numpy(x) if host else x, dv.to_numpy(r) if host else r)
+            break
+        beta = 0.0 if it == 1 else rtz / rtz_old
+        check(lib.sem_add2s1(dv.ptr(p), dv.ptr(r), beta, m, s), "add2s1")
+        w = operator(dv.to_numpy(p) if host else p)
+        w = dv.as_device_f64(w, dev, "operator output")
+        pap = dot(p, w)
+        if pap <= 0.0:
+            ppc = dot(p, p)
+            raise CgBreakdownError(
+                f"<p, A p>_c = {pap:.3e} at iteration {it} "
+                f"(scale <p, p>_c = {ppc:.3e}); operator is not SPD here")
+        alpha = rtz / pap
+        check(lib.sem_add2s2(dv.ptr(x), dv.ptr(p), alpha, m, s), "add2s2")
+        check(lib.sem_add2s2(dv.ptr(r), dv.ptr(w), -alpha, m, s), "add2s2")
+        rnorm = math.sqrt(dot(r, r))
+        history.append(rnorm)
+        iters = it
+        counters.add(reads=(9 + 6) * dofs, writes=3 * dofs,
+                     flops=CG_VECTOR_FLOPS_PER_POINT * dofs)
+        if callback is not None:
+            callback(it, dv.to_numpy(x) if host else x, dv.to_numpy(r) if host else r)
+        if cfg.tolerance > 0.0 and rnorm < cfg.tolerance:
+            break
+    if zero_exit:
+        counters.add(reads=3 * dofs, flops=2 * dofs)
+    return x, np.asarray(history, dtype=np.float64), iters
+
+
+def cg_solve(f, operator, topo: Topology, cfg: CgConfig,
+             counters: TrafficCounters | None = None, callback=None,
+             workspace: CgWorkspace | None = None) -> CgResult:
+    """Run CG on A x = f (reference recurrence, cg.py:139-186)."""
+    if counters is None:
+        counters = TrafficCounters()
+    validate_field(f, topo.num_elements, topo.n, "f")
+    fd, kind = dv.to_device_io(f, "f")
+    host = kind != "device"
+    dofs = topo.dofs
+    # r = mask(f) on entry (cg.py:139)
+    counters.add(reads=2 * dofs, writes=dofs)
+    with torch.cuda.device(fd.device):
+        if isinstance(operator, GlobalOperator) and operator.topo == topo:
+            x, history, iters, zero_exit = _fused_solve(fd, operator, topo, cfg, callback, host,
+                                                        workspace)
+            full = iters - (1 if zero_exit else 0)
+            counters.add(reads=15 * dofs * full, writes=3 * dofs * full,
+                         flops=CG_VECTOR_FLOPS_PER_POINT * dofs * full)
+            if zero_exit:
+                counters.add(reads=3 * dofs, flops=2 * dofs)
+            operator.account(full)
+        else:
+            x, history, iters = _generic_solve(fd, operator, topo, cfg, counters, callback, host)
+    return CgResult(solution=dv.from_device_io(x, kind), residual_history=history,
+                    iterations_run=iters, counters=counters.copy())

@@ -1,0 +1,309 @@
+// Local Poisson operator Ax on B200 (sm_100a), FP64.
+//
+// Algorithm: the LAYERED variant of sembench/kernels.py:267-410 (paper
+// §IV-C): a 2-D layer of threads walks the k layers of an element in lock
+// step; each thread keeps its u column and its w accumulator column in
+// registers, the r/s contractions of a layer read the layer (and its
+// phase-1 results) from shared memory, and the t contraction is a register
+// GEMV whose D entries are compile-time constant-bank operands.
+//
+// B200-specific layout decisions:
+//  * a thread owns an i-PAIR (i0, i0+1) of one (j) row, so every u / g / w
+//    global access is a coalesced 128-bit vector (ld.global.nc.v2.f64) and
+//    every shared-memory read of the layer is an LDS.128; odd n pads the
+//    shared layer to an even row stride with a zero phantom column.
+//  * D and D^T live in shared memory for the lane-varying (r, s) directions
+//    and in kernel-parameter constant space for the warp-uniform (t)
+//    direction -- so the t-direction costs no shared-memory traffic.
+//  * several elements ("slots") per CTA, double-buffered layer arrays so a
+//    layer needs two CTA barriers, and the next layer's six metric vectors
+//    are prefetched into registers while the current one computes.
+//
+// Arithmetic differs from the reference only by FMA contraction and
+// association (tolerance 1e-12 max-norm relative, sembench/verify.py:37-42).
+#include "sem_common.cuh"
+
+namespace sem {
+
+template <int N>
+struct DParam {
+    double d[N * N];  // D[i][l] row-major (basis.diff)
+};
+
+__device__ __forceinline__ double2 ldg2(const double* p)
+{
+    double2 v;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ldg1(const double* p)
+{
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void stg2(double* p, double2 v)
+{
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Compile-time configuration per n.
+template <int N>
+struct AxCfg {
+    static constexpr int NE = (N + 1) & ~1;        // padded row length (even)
+    static constexpr int NP = NE / 2;              // i-pairs per row
+    static constexpr int TPE = NP * N;             // threads per element
+    static constexpr int NN = N * N;
+    static constexpr int NNN = N * N * N;
+    static constexpr int LAYER = NE * N;           // padded layer size (doubles)
+    // elements per CTA: aim at ~256-448 threads
+    static constexpr int SLOTS = (TPE >= 256) ? 1 : ((448 / TPE) < 1 ? 1 : (448 / TPE));
+    static constexpr int THREADS = ((SLOTS * TPE + 31) / 32) * 32;
+    static constexpr bool VEC = (N % 2) == 0;      // 16-B aligned global pairs
+};
+
+template <int N, int SLOTS>
+struct AxSmem {
+    static constexpr int NE = AxCfg<N>::NE;
+    static constexpr int LAYER = AxCfg<N>::LAYER;
+    alignas(16) double d[N * NE];    // d[i*NE + l]  = D[i][l]   (pad l>=N with 0)
+    alignas(16) double dt[NE * NE];  // dt[l*NE + i] = D[i][l]   (pad i>=N with 0)
+    alignas(16) double u[2][SLOTS][LAYER];
+    alignas(16) double r[2][SLOTS][LAYER];
+    alignas(16) double s[2][SLOTS][LAYER];
+};
+
+template <int N, int SLOTS, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+ax_layered_kernel(const double* __restrict__ u, const double* __restrict__ g,
+                  double* __restrict__ w, int64_t num_elements, const DParam<N> D)
+{
+    using C = AxCfg<N>;
+    constexpr int NE = C::NE, NP = C::NP, TPE = C::TPE, NN = C::NN, NNN = C::NNN;
+    constexpr bool VEC = C::VEC;
+    __shared__ AxSmem<N, SLOTS> sm;
+
+    const int tid = threadIdx.x;
+    // D tables (padded with zeros so phantom rows/columns contribute 0)
+    for (int t = tid; t < N * NE; t += THREADS) {
+        const int i = t / NE, l = t % NE;
+        sm.d[t] = (l < N) ? D.d[i * N + l] : 0.0;
+    }
+    for (int t = tid; t < NE * NE; t += THREADS) {
+        const int l = t / NE, i = t % NE;
+        sm.dt[t] = (i < N && l < N) ? D.d[i * N + l] : 0.0;
+    }
+
+    const int slot = tid / TPE;
+    const int rem = tid - slot * TPE;
+    const int j = rem / NP;
+    const int i0 = 2 * (rem - j * NP);
+    const int64_t e = (int64_t)blockIdx.x * SLOTS + slot;
+    const bool active = (slot < SLOTS) && (e < num_elements);
+    const bool second = (i0 + 1) < N;  // false only for the phantom of odd n
+    const int sl = active ? slot : 0;
+
+    const double* ue = u + (active ? e : 0) * NNN + j * N + i0;
+    const double* ge = g + (active ? e : 0) * (6 * NNN) + j * N + i0;
+
+    // u column of the pair, all layers (coalesced 128-bit loads)
+    double2 uc[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        if (!active) {
+            uc[k] = make_double2(0.0, 0.0);
+        } else if (VEC) {
+            uc[k] = ldg2(ue + k * NN);
+        } else {
+            uc[k].x = ldg1(ue + k * NN);
+            uc[k].y = second ? ldg1(ue + k * NN + 1) : 0.0;
+        }
+    }
+    double2 acc[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) acc[k] = make_double2(0.0, 0.0);
+
+    auto load_g = [&](double2 (&gv)[6], int k) {
+#pragma unroll
+        for (int m = 0; m < 6; ++m) {
+            const double* p = ge + m * NNN + k * NN;
+            if (!active) {
+                gv[m] = make_double2(0.0, 0.0);
+            } else if (VEC) {
+                gv[m] = ldg2(p);
+            } else {
+                gv[m].x = ldg1(p);
+                gv[m].y = second ? ldg1(p + 1) : 0.0;
+            }
+        }
+    };
+    double2 gn[6];
+    load_g(gn, 0);
+    __syncthreads();
+
+    const double2* d2 = reinterpret_cast<const double2*>(sm.d);
+    const double2* dt2 = reinterpret_cast<const double2*>(sm.dt);
+
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const int b = k & 1;
+        double* su = sm.u[b][sl];
+        double* sr = sm.r[b][sl];
+        double* ss = sm.s[b][sl];
+        if (active) *reinterpret_cast<double2*>(su + j * NE + i0) = uc[k];
+        double2 gc[6];
+#pragma unroll
+        for (int m = 0; m < 6; ++m) gc[m] = gn[m];
+        if (k + 1 < N) load_g(gn, k + 1);
+        __syncthreads();
+
+        // ---- phase 1: directional derivatives at layer k ----
+        const double2* su2 = reinterpret_cast<const double2*>(su);
+        double wr0 = 0.0, wr1 = 0.0, ws0 = 0.0, ws1 = 0.0, wt0 = 0.0, wt1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const double2 ur = su2[(j * NE) / 2 + q];                 // U[j][2q..2q+1]
+            const double2 da = dt2[((2 * q) * NE + i0) / 2];          // D[i0..i0+1][2q]
+            const double2 dj = d2[(j * NE) / 2 + q];                  // D[j][2q..2q+1]
+            const double2 ua = su2[((2 * q) * NE + i0) / 2];          // U[2q][i0..i0+1]
+            wr0 = fma(da.x, ur.x, wr0);
+            wr1 = fma(da.y, ur.x, wr1);
+            ws0 = fma(dj.x, ua.x, ws0);
+            ws1 = fma(dj.x, ua.y, ws1);
+            if (2 * q + 1 < N) {
+                const double2 db = dt2[((2 * q + 1) * NE + i0) / 2];  // D[i0..][2q+1]
+                const double2 ub = su2[((2 * q + 1) * NE + i0) / 2];  // U[2q+1][i0..]
+                wr0 = fma(db.x, ur.y, wr0);
+                wr1 = fma(db.y, ur.y, wr1);
+                ws0 = fma(dj.y, ub.x, ws0);
+                ws1 = fma(dj.y, ub.y, ws1);
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < N; ++l) {
+            const double dkl = D.d[k * N + l];  // warp-uniform: constant bank
+            wt0 = fma(dkl, uc[l].x, wt0);
+            wt1 = fma(dkl, uc[l].y, wt1);
+        }
+        // metric: (ur,us,ut) = G (wr,ws,wt), G = (g1 g2 g3; g2 g4 g5; g3 g5 g6)
+        const double r0 = fma(gc[2].x, wt0, fma(gc[1].x, ws0, gc[0].x * wr0));
+        const double r1 = fma(gc[2].y, wt1, fma(gc[1].y, ws1, gc[0].y * wr1));
+        const double s0 = fma(gc[4].x, wt0, fma(gc[3].x, ws0, gc[1].x * wr0));
+        const double s1 = fma(gc[4].y, wt1, fma(gc[3].y, ws1, gc[1].y * wr1));
+        const double t0 = fma(gc[5].x, wt0, fma(gc[4].x, ws0, gc[2].x * wr0));
+        const double t1 = fma(gc[5].y, wt1, fma(gc[4].y, ws1, gc[2].y * wr1));
+        if (active) {
+            *reinterpret_cast<double2*>(sr + j * NE + i0) = make_double2(r0, r1);
+            *reinterpret_cast<double2*>(ss + j * NE + i0) = make_double2(s0, s1);
+        }
+        __syncthreads();
+
+        // ---- phase 2: transposed contractions ----
+        const double2* sr2 = reinterpret_cast<const double2*>(sr);
+        const double2* ss2 = reinterpret_cast<const double2*>(ss);
+        double ar0 = 0.0, ar1 = 0.0, as0 = 0.0, as1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const double2 rr = sr2[(j * NE) / 2 + q];                 // ur[j][2q..]
+            const double2 da = d2[((2 * q) * NE + i0) / 2];           // D[2q][i0..i0+1]
+            const double2 dj = dt2[(j * NE) / 2 + q];                 // D[2q..2q+1][j]
+            const double2 sa = ss2[((2 * q) * NE + i0) / 2];          // us[2q][i0..]
+            ar0 = fma(da.x, rr.x, ar0);
+            ar1 = fma(da.y, rr.x, ar1);
+            as0 = fma(dj.x, sa.x, as0);
+            as1 = fma(dj.x, sa.y, as1);
+            if (2 * q + 1 < N) {
+                const double2 db = d2[((2 * q + 1) * NE + i0) / 2];   // D[2q+1][i0..]
+                const double2 sb = ss2[((2 * q + 1) * NE + i0) / 2];
+                ar0 = fma(db.x, rr.y, ar0);
+                ar1 = fma(db.y, rr.y, ar1);
+                as0 = fma(dj.y, sb.x, as0);
+                as1 = fma(dj.y, sb.y, as1);
+            }
+        }
+        acc[k].x += ar0 + as0;
+        acc[k].y += ar1 + as1;
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk) {
+            const double dkk = D.d[k * N + kk];  // D^T[kk][k]
+            acc[kk].x = fma(dkk, t0, acc[kk].x);
+            acc[kk].y = fma(dkk, t1, acc[kk].y);
+        }
+    }
+
+    if (active) {
+        double* we = w + e * NNN + j * N + i0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            if (VEC) {
+                stg2(we + k * NN, acc[k]);
+            } else {
+                we[k * NN] = acc[k].x;
+                if (second) we[k * NN + 1] = acc[k].y;
+            }
+        }
+    }
+}
+
+template <int N>
+static int launch_ax(const double* u, const double* g, const double* dx, double* w,
+                     int64_t E, cudaStream_t stream)
+{
+    using C = AxCfg<N>;
+    DParam<N> D;
+    for (int t = 0; t < N * N; ++t) D.d[t] = dx[t];
+    if (E == 0) return 0;
+    const int64_t blocks = (E + C::SLOTS - 1) / C::SLOTS;
+    if (blocks > 0x7fffffffLL) {
+        set_error("sem_ax: too many elements (%lld)", (long long)E);
+        return SEM_E_INVALID;
+    }
+    ax_layered_kernel<N, C::SLOTS, C::THREADS>
+        <<<(unsigned)blocks, C::THREADS, 0, stream>>>(u, g, w, E, D);
+    SEM_CHECK_LAUNCH("sem_ax launch");
+    return 0;
+}
+
+int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
+                int n, int variant, cudaStream_t stream)
+{
+    (void)variant;
+    switch (n) {
+#define SEM_AX_CASE(NV) \
+    case NV: return launch_ax<NV>(u, g, dx, w, E, stream);
+        SEM_AX_CASE(2) SEM_AX_CASE(3) SEM_AX_CASE(4) SEM_AX_CASE(5) SEM_AX_CASE(6)
+        SEM_AX_CASE(7) SEM_AX_CASE(8) SEM_AX_CASE(9) SEM_AX_CASE(10) SEM_AX_CASE(11)
+        SEM_AX_CASE(12) SEM_AX_CASE(13) SEM_AX_CASE(14) SEM_AX_CASE(15) SEM_AX_CASE(16)
+#undef SEM_AX_CASE
+        default:
+            set_error("sem_ax: n=%d outside the supported range [2, 16]", n);
+            return SEM_E_INVALID;
+    }
+}
+
+}  // namespace sem
+
+extern "C" int sem_ax_variant(const double* u, const double* g, const double* dx,
+                              const double* dxt, double* w, int64_t num_elements,
+                              int32_t n, int32_t variant, sem_stream_t stream)
+{
+    if (!u || !g || !dx || !dxt || !w || num_elements < 0) {
+        sem::set_error("sem_ax: null pointer or negative element count");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = sem::bind_stream_device(s)) return rc;
+    return sem::ax_dispatch(u, g, dx, w, num_elements, n, variant, s);
+}
+
+extern "C" int sem_ax(const double* u, const double* g, const double* dx,
+                      const double* dxt, double* w, int64_t num_elements, int32_t n,
+                      sem_stream_t stream)
+{
+    return sem_ax_variant(u, g, dx, dxt, w, num_elements, n, 0, stream);
+}
+
+extern "C" int sem_ax_num_variants(int32_t n)
+{
+    return (n >= 2 && n <= 16) ? 1 : 0;
+}

@@ -1,0 +1,361 @@
+// CG vector kernels (Nekbone add2s1 / add2s2 / glsc3) and the fused,
+// device-resident CG iteration of sembench/cg.py:114-193.
+//
+// * add2s1 / add2s2 are bit-exact restatements of _scale_add / _axpy_into
+//   (cg.py:95-104): multiply rounded, then add rounded (no FMA).
+// * glsc3 is a deterministic fixed-tree reduction (reduce.cuh); on the box
+//   the weight 1/multiplicity is recomputed from the lattice, so the three
+//   weighted dots of an iteration read 2 streams instead of 3.
+// * The CG driver keeps rtz / pap / alpha / beta in a device-side
+//   sem_cg_state: an iteration is four launches (p-update, Ax, dssum+mask
+//   fused with <p,w>_c, x/r-update fused with <r,r>_c) with no host
+//   synchronisation; early exits (rtz == 0, tolerance, breakdown) set a
+//   device stop flag that turns the remaining queued launches into no-ops.
+#include <math.h>
+
+#include <algorithm>
+
+#include "box.cuh"
+#include "reduce.cuh"
+
+namespace sem {
+
+int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
+                int n, int variant, cudaStream_t stream);
+
+constexpr int kVecThreads = 256;
+
+static unsigned vec_grid(int64_t pairs)
+{
+    const int64_t per = (int64_t)kVecThreads;
+    int64_t b = (pairs + per - 1) / per;
+    const int64_t cap = 16LL * sm_count();
+    if (b > cap) b = cap;
+    return (unsigned)(b > 0 ? b : 1);
+}
+
+// ---------------------------------------------------------- add2s1/add2s2 --
+__global__ void __launch_bounds__(kVecThreads)
+add2s1_kernel(double* __restrict__ p, const double* __restrict__ z, double beta, int64_t m)
+{
+    const int64_t stride = (int64_t)gridDim.x * kVecThreads;
+    for (int64_t q = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; q < m; q += stride)
+        p[q] = add_rn(mul_rn(beta, p[q]), __ldg(z + q));
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+add2s2_kernel(double* __restrict__ x, const double* __restrict__ y, double alpha, int64_t m)
+{
+    const int64_t stride = (int64_t)gridDim.x * kVecThreads;
+    for (int64_t q = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; q < m; q += stride)
+        x[q] = add_rn(x[q], mul_rn(alpha, __ldg(y + q)));
+}
+
+// ------------------------------------------------------------- glsc3 -----
+__global__ void __launch_bounds__(kReduceThreads)
+glsc3_kernel(const double* __restrict__ a, const double* __restrict__ b,
+             const double* __restrict__ wt, int64_t m, double* out, ReduceScratch* rs)
+{
+    double acc = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kReduceThreads;
+    for (int64_t q = (int64_t)blockIdx.x * kReduceThreads + threadIdx.x; q < m; q += stride)
+        acc += mul_rn(mul_rn(__ldg(a + q), __ldg(b + q)), __ldg(wt + q));
+    const double vals[1] = {acc};
+    reduce_publish_and_finish<1, kReduceThreads>(vals, rs, [&](const double (&t)[1]) { *out = t[0]; });
+}
+
+// Box-weighted dot: one element per block iteration so the lattice
+// coordinate is computed once; w = 1/multiplicity from the lattice.  The
+// loop nest (and so the summation order) is shared with the fused CG
+// kernels below, so weighted_dot reproduces their reductions bit-for-bit.
+template <int N>
+__global__ void __launch_bounds__(kReduceThreads)
+glsc3_box_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t E, Box bx,
+                 double* out, ReduceScratch* rs)
+{
+    constexpr int NN = N * N, NNN = N * N * N;
+    double acc = 0.0;
+    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        const ElemCoord c = elem_coord(e, bx);
+        for (int q = threadIdx.x; q < NNN; q += kReduceThreads) {
+            const int k = q / NN, j = (q / N) % N, i = q % N;
+            const int64_t idx = e * NNN + q;
+            acc += mul_rn(mul_rn(__ldg(a + idx), __ldg(b + idx)), inv_mult<N>(c, i, j, k, bx));
+        }
+    }
+    const double vals[1] = {acc};
+    reduce_publish_and_finish<1, kReduceThreads>(vals, rs, [&](const double (&t)[1]) { *out = t[0]; });
+}
+
+// ------------------------------------------------------------ CG kernels --
+// init: r = mask(f) (assembly.py:123-129), x = p = 0, rtz = <r,r>_c.
+template <int N>
+__global__ void __launch_bounds__(kReduceThreads)
+cg_init_kernel(const double* __restrict__ f, double* __restrict__ x, double* __restrict__ r,
+               double* __restrict__ p, int64_t E, Box bx, sem_cg_state* st, ReduceScratch* rs,
+               int max_iterations, double tolerance)
+{
+    constexpr int NN = N * N, NNN = N * N * N;
+    double acc = 0.0;
+    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        const ElemCoord c = elem_coord(e, bx);
+        for (int q = threadIdx.x; q < NNN; q += kReduceThreads) {
+            const int k = q / NN, j = (q / N) % N, i = q % N;
+            const int64_t idx = e * NNN + q;
+            const double rv = mul_rn(__ldg(f + idx), mask_val<N>(c, i, j, k, bx));
+            r[idx] = rv;
+            x[idx] = 0.0;
+            p[idx] = 0.0;
+            acc += mul_rn(mul_rn(rv, rv), inv_mult<N>(c, i, j, k, bx));
+        }
+    }
+    const double vals[1] = {acc};
+    reduce_publish_and_finish<1, kReduceThreads>(vals, rs, [&](const double (&t)[1]) {
+        st->rtz = t[0];
+        st->rtz_old = 1.0;  // cg.py:146 (unused: beta = 0 on iteration 1)
+        st->pap = 0.0;
+        st->alpha = 0.0;
+        st->beta = 0.0;
+        st->it = 0;
+        st->iterations_run = 0;
+        st->stop = 0;
+        st->breakdown_it = 0;
+        st->max_iterations = max_iterations;
+        st->tolerance = tolerance;
+    });
+}
+
+// Top of an iteration (cg.py:149-160): exact-zero exit, beta, p = beta p + r.
+__global__ void __launch_bounds__(kVecThreads)
+cg_p_kernel(double* __restrict__ p, const double* __restrict__ r, int64_t m, sem_cg_state* st,
+            double* history)
+{
+    if (st->stop) return;
+    const int it = st->it + 1;
+    const double rtz = st->rtz;
+    if (rtz == 0.0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            history[it - 1] = 0.0;
+            st->iterations_run = it;
+            st->stop = 1;
+        }
+        return;
+    }
+    const double beta = (it == 1) ? 0.0 : rtz / st->rtz_old;
+    const int64_t stride = (int64_t)gridDim.x * kVecThreads;
+    for (int64_t q = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; q < m; q += stride)
+        p[q] = add_rn(mul_rn(beta, p[q]), __ldg(r + q));
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->beta = beta;
+}
+
+// w2 = mask(dssum(w)) and <p, w2>_c (assembly.py:113-129 + cg.py:163-170).
+template <int N>
+__global__ void __launch_bounds__(kReduceThreads)
+cg_assemble_kernel(const double* __restrict__ w, double* __restrict__ w2,
+                   const double* __restrict__ p, int64_t E, Box bx, sem_cg_state* st,
+                   ReduceScratch* rs)
+{
+    constexpr int NN = N * N, NNN = N * N * N;
+    if (st->stop) return;
+    double acc = 0.0;
+    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        const ElemCoord c = elem_coord(e, bx);
+        for (int q = threadIdx.x; q < NNN; q += kReduceThreads) {
+            const int k = q / NN, j = (q / N) % N, i = q % N;
+            const int64_t idx = e * NNN + q;
+            const double v = mul_rn(gather_sum<N>(w, c, i, j, k, bx), mask_val<N>(c, i, j, k, bx));
+            w2[idx] = v;
+            acc += mul_rn(mul_rn(__ldg(p + idx), v), inv_mult<N>(c, i, j, k, bx));
+        }
+    }
+    const double vals[1] = {acc};
+    reduce_publish_and_finish<1, kReduceThreads>(vals, rs, [&](const double (&t)[1]) {
+        const double pap = t[0];
+        st->pap = pap;
+        if (pap <= 0.0) {
+            st->stop = 2;
+            st->breakdown_it = st->it + 1;
+        } else {
+            st->alpha = st->rtz / pap;
+        }
+    });
+}
+
+// x += alpha p ; r += (-alpha) w2 ; rnorm = sqrt(<r,r>_c)  (cg.py:170-186).
+template <int N>
+__global__ void __launch_bounds__(kReduceThreads)
+cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                 const double* __restrict__ w2, int64_t E, Box bx, sem_cg_state* st,
+                 double* history, ReduceScratch* rs)
+{
+    constexpr int NN = N * N, NNN = N * N * N;
+    if (st->stop) return;
+    const double alpha = st->alpha, nalpha = -alpha;
+    double acc = 0.0;
+    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+        const ElemCoord c = elem_coord(e, bx);
+        for (int q = threadIdx.x; q < NNN; q += kReduceThreads) {
+            const int k = q / NN, j = (q / N) % N, i = q % N;
+            const int64_t idx = e * NNN + q;
+            x[idx] = add_rn(x[idx], mul_rn(alpha, __ldg(p + idx)));
+            const double rv = add_rn(r[idx], mul_rn(nalpha, __ldg(w2 + idx)));
+            r[idx] = rv;
+            acc += mul_rn(mul_rn(rv, rv), inv_mult<N>(c, i, j, k, bx));
+        }
+    }
+    const double vals[1] = {acc};
+    reduce_publish_and_finish<1, kReduceThreads>(vals, rs, [&](const double (&t)[1]) {
+        const double rtr = t[0];
+        const int it = st->it + 1;
+        const double rnorm = sqrt(rtr);
+        history[it - 1] = rnorm;
+        st->iterations_run = it;
+        st->rtz_old = st->rtz;
+        st->rtz = rtr;   // equals <r,r>_c at the top of the next iteration
+        st->it = it;
+        if (st->tolerance > 0.0 && rnorm < st->tolerance) st->stop = 3;
+    });
+}
+
+static unsigned red_grid(int64_t E)
+{
+    return (unsigned)(E < kReduceBlocks ? (E > 0 ? E : 1) : kReduceBlocks);
+}
+
+template <int N>
+static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_state* st,
+                     int64_t E, Box bx, ReduceScratch* rs, int max_it, double tol,
+                     cudaStream_t s)
+{
+    cg_init_kernel<N><<<red_grid(E), kReduceThreads, 0, s>>>(f, x, r, p, E, bx, st, rs,
+                                                              max_it, tol);
+    SEM_CHECK_LAUNCH("sem_cg_init launch");
+    return 0;
+}
+
+template <int N>
+static int cg_run_n(const double* g, const double* dx, double* x, double* r, double* p,
+                    double* w, double* w2, sem_cg_state* st, double* history, int iters,
+                    int64_t E, Box bx, ReduceScratch* rs, cudaStream_t s)
+{
+    constexpr int NNN = N * N * N;
+    const int64_t m = E * NNN;
+    for (int it = 0; it < iters; ++it) {
+        cg_p_kernel<<<vec_grid(m), kVecThreads, 0, s>>>(p, r, m, st, history);
+        SEM_CHECK_LAUNCH("cg_p_kernel");
+        if (int rc = ax_dispatch(p, g, dx, w, E, N, 0, s)) return rc;
+        cg_assemble_kernel<N><<<red_grid(E), kReduceThreads, 0, s>>>(w, w2, p, E, bx, st, rs);
+        SEM_CHECK_LAUNCH("cg_assemble_kernel");
+        cg_update_kernel<N><<<red_grid(E), kReduceThreads, 0, s>>>(x, r, p, w2, E, bx, st,
+                                                                    history, rs);
+        SEM_CHECK_LAUNCH("cg_update_kernel");
+    }
+    return 0;
+}
+
+}  // namespace sem
+
+using namespace sem;
+
+extern "C" int64_t sem_reduce_scratch_bytes(void) { return (int64_t)sizeof(ReduceScratch); }
+
+extern "C" int sem_add2s1(double* p, const double* z, double beta, int64_t m, sem_stream_t stream)
+{
+    if (!p || !z || m < 0) { set_error("sem_add2s1: bad arguments"); return SEM_E_INVALID; }
+    if (m == 0) return 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    add2s1_kernel<<<vec_grid(m), kVecThreads, 0, s>>>(p, z, beta, m);
+    SEM_CHECK_LAUNCH("sem_add2s1 launch");
+    return 0;
+}
+
+extern "C" int sem_add2s2(double* x, const double* y, double alpha, int64_t m, sem_stream_t stream)
+{
+    if (!x || !y || m < 0) { set_error("sem_add2s2: bad arguments"); return SEM_E_INVALID; }
+    if (m == 0) return 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    add2s2_kernel<<<vec_grid(m), kVecThreads, 0, s>>>(x, y, alpha, m);
+    SEM_CHECK_LAUNCH("sem_add2s2 launch");
+    return 0;
+}
+
+extern "C" int sem_glsc3(const double* a, const double* b, const double* wt, int64_t m,
+                         double* out_dev, void* scratch, sem_stream_t stream)
+{
+    if (!a || !b || !wt || !out_dev || !scratch || m < 0) {
+        set_error("sem_glsc3: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const unsigned grid = (unsigned)std::min<int64_t>(
+        kReduceBlocks, std::max<int64_t>(1, (m + kReduceThreads - 1) / kReduceThreads));
+    glsc3_kernel<<<grid, kReduceThreads, 0, s>>>(a, b, wt, m, out_dev,
+                                                 static_cast<ReduceScratch*>(scratch));
+    SEM_CHECK_LAUNCH("sem_glsc3 launch");
+    return 0;
+}
+
+extern "C" int sem_glsc3_box(const double* a, const double* b, int32_t ex, int32_t ey,
+                             int32_t ez, int32_t n, double* out_dev, void* scratch,
+                             sem_stream_t stream)
+{
+    if (int rc = check_box(ex, ey, ez, n, "sem_glsc3_box")) return rc;
+    if (!a || !b || !out_dev || !scratch) { set_error("sem_glsc3_box: null pointer"); return SEM_E_INVALID; }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const Box bx{ex, ey, ez, 0, ez};
+    const int64_t E = (int64_t)ex * ey * ez;
+    auto* rs = static_cast<ReduceScratch*>(scratch);
+    SEM_SWITCH_N(n, {
+        glsc3_box_kernel<NV><<<red_grid(E), kReduceThreads, 0, s>>>(a, b, E, bx, out_dev, rs);
+        SEM_CHECK_LAUNCH("sem_glsc3_box launch");
+        return 0;
+    });
+}
+
+extern "C" int sem_cg_init(const double* f, double* x, double* r, double* p, sem_cg_state* state,
+                           double* history, int32_t max_iterations, double tolerance,
+                           int32_t ex, int32_t ey, int32_t ez, int32_t n, void* scratch,
+                           sem_stream_t stream)
+{
+    if (int rc = check_box(ex, ey, ez, n, "sem_cg_init")) return rc;
+    if (!f || !x || !r || !p || !state || !history || !scratch || max_iterations < 1 ||
+        tolerance < 0.0) {
+        set_error("sem_cg_init: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const Box bx{ex, ey, ez, 0, ez};
+    const int64_t E = (int64_t)ex * ey * ez;
+    auto* rs = static_cast<ReduceScratch*>(scratch);
+    SEM_SWITCH_N(n, return cg_init_n<NV>(f, x, r, p, state, E, bx, rs, max_iterations,
+                                         tolerance, s));
+}
+
+extern "C" int sem_cg_run(const double* g, const double* dx, const double* dxt, double* x,
+                          double* r, double* p, double* w, sem_cg_state* state, double* history,
+                          int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+                          void* scratch, sem_stream_t stream)
+{
+    (void)dxt;
+    if (int rc = check_box(ex, ey, ez, n, "sem_cg_run")) return rc;
+    if (!g || !dx || !x || !r || !p || !w || !state || !history || !scratch || iterations < 0) {
+        set_error("sem_cg_run: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const Box bx{ex, ey, ez, 0, ez};
+    const int64_t E = (int64_t)ex * ey * ez;
+    const int64_t m = E * n * n * n;
+    auto* rs = static_cast<ReduceScratch*>(scratch);
+    // w holds two E*n^3 vectors: local Ax output, then the assembled field
+    double* w_local = w;
+    double* w_asm = w + m;
+    SEM_SWITCH_N(n, return cg_run_n<NV>(g, dx, x, r, p, w_local, w_asm, state, history,
+                                        iterations, E, bx, rs, s));
+}

@@ -1,0 +1,63 @@
+// Error state, device binding and ABI metadata for libsem.
+#include <stdarg.h>
+#include <string.h>
+
+#include "sem_common.cuh"
+
+namespace sem {
+
+static thread_local char g_last_error[512] = "";
+
+void set_error(const char* fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+    va_end(ap);
+}
+
+int fail_cuda(cudaError_t err, const char* what)
+{
+    set_error("%s: %s (%s)", what, cudaGetErrorString(err), cudaGetErrorName(err));
+    return static_cast<int>(err);
+}
+
+int bind_stream_device(cudaStream_t stream)
+{
+    // The legacy/per-thread default streams belong to the current device.
+    if (stream == nullptr || stream == cudaStreamLegacy || stream == cudaStreamPerThread)
+        return 0;
+    static thread_local cudaStream_t last_stream = nullptr;
+    static thread_local int last_device = -1;
+    int dev = last_device;
+    if (stream != last_stream || dev < 0) {
+        cudaError_t err = cudaStreamGetDevice(stream, &dev);
+        if (err != cudaSuccess) return fail_cuda(err, "cudaStreamGetDevice");
+        last_stream = stream;
+        last_device = dev;
+    }
+    int cur = -1;
+    cudaError_t err = cudaGetDevice(&cur);
+    if (err != cudaSuccess) return fail_cuda(err, "cudaGetDevice");
+    if (cur != dev) {
+        err = cudaSetDevice(dev);
+        if (err != cudaSuccess) return fail_cuda(err, "cudaSetDevice");
+    }
+    return 0;
+}
+
+int sm_count()
+{
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMsB200;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+        return kNumSMsB200;
+    return n;
+}
+
+}  // namespace sem
+
+extern "C" int sem_abi_version(void) { return SEM_ABI_VERSION; }
+extern "C" const char* sem_last_error(void) { return sem::g_last_error; }
+extern "C" int sem_min_points(void) { return 2; }
+extern "C" int sem_max_points(void) { return 16; }

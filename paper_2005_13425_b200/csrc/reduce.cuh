@@ -1,0 +1,86 @@
+// Deterministic two-stage reductions (fixed grid, fixed tree order).
+//
+// The reference's glsc3 (sembench/cg.py:77-92) folds 65536-point chunks
+// sequentially; replicating that order on a GPU would serialise 65536-long
+// dependency chains, so the device instead uses a FIXED reduction tree: a
+// constant number of blocks (kReduceBlocks, independent of the GPU), a fixed
+// per-thread stride pattern, a warp-shuffle tree and an in-order combine of
+// block partials by the last block to finish.  Results are bit-reproducible
+// run to run and across devices, and agree with the reference to rounding.
+#pragma once
+#include "sem_common.cuh"
+
+namespace sem {
+
+constexpr int kReduceBlocks = 296;   // 2 x 148; a constant so the tree is fixed
+constexpr int kReduceThreads = 256;
+constexpr int kMaxReductions = 4;    // independent accumulators per kernel
+
+// scratch layout: double partials[kMaxReductions][kReduceBlocks]; uint32 counter
+struct ReduceScratch {
+    double partials[kMaxReductions][kReduceBlocks];
+    unsigned int counter;
+    unsigned int pad[15];
+};
+
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// Block-wide sum in a fixed order; result valid in thread 0.
+template <int THREADS>
+__device__ __forceinline__ double block_sum(double v, double* sh /* >= THREADS/32 */)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (wid == 0) {
+        t = (lane < THREADS / 32) ? sh[lane] : 0.0;
+        t = warp_sum(t);
+    }
+    __syncthreads();
+    return t;
+}
+
+// Publish NR block partials; the last block to arrive combines them in
+// block order and calls fin(totals) from thread 0.  Returns true in the
+// finishing block.
+template <int NR, int THREADS, typename Fin>
+__device__ __forceinline__ void reduce_publish_and_finish(const double (&vals)[NR],
+                                                          ReduceScratch* rs, Fin fin)
+{
+    __shared__ double sh[THREADS / 32];
+    __shared__ bool am_last;
+    double tot[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) tot[q] = block_sum<THREADS>(vals[q], sh);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < NR; ++q) rs->partials[q][blockIdx.x] = tot[q];
+        __threadfence();
+        const unsigned prev = atomicAdd(&rs->counter, 1u);
+        am_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    double fin_tot[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+        double v = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += THREADS)
+            v += __ldcg(&rs->partials[q][b]);
+        fin_tot[q] = block_sum<THREADS>(v, sh);
+    }
+    if (threadIdx.x == 0) {
+        rs->counter = 0u;
+        fin(fin_tot);
+    }
+}
+
+}  // namespace sem

@@ -1,0 +1,46 @@
+// Shared helpers for libsem (B200 / sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/sem.h"
+
+namespace sem {
+
+// Error reporting: every C-ABI entry point returns 0 on success, else a
+// cudaError_t (or SEM_E_* code) and leaves a message for sem_last_error().
+void set_error(const char* fmt, ...);
+int fail_cuda(cudaError_t err, const char* what);
+
+// Make the calling thread's runtime device match the device owning `stream`
+// (the library links cudart statically, so its current-device state is
+// separate from torch's).
+int bind_stream_device(cudaStream_t stream);
+
+constexpr int kNumSMsB200 = 148;
+int sm_count();
+
+// Analytic structured-box helpers (sembench/assembly.py:69-110): element
+// e = ex_i + ex*(ey_i + ey*ez_i); global lattice coordinate along x is
+// ex_i*(n-1)+i, and a node is interior iff every coordinate is strictly inside
+// the global point grid [0, ex*(n-1)].
+struct BoxDims {
+    int ex, ey, ez;   // elements per axis of THIS field (a z-slab for multi-GPU)
+    int n;
+    int gz0;          // global element-layer offset of this slab along z
+    int ez_global;    // global element count along z
+};
+
+}  // namespace sem
+
+#define SEM_CHECK_LAUNCH(what)                                         \
+    do {                                                               \
+        cudaError_t _e = cudaGetLastError();                           \
+        if (_e != cudaSuccess) return ::sem::fail_cuda(_e, what);      \
+    } while (0)
+
+// IEEE double ops that nvcc must not contract into FMA: the reference's
+// vector updates are unfused multiply-then-add (sembench/cg.py:95-104).
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }

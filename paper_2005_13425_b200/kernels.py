@@ -1,0 +1,144 @@
+"""Element-local Poisson operator ``apply_ax`` on the B200 (contract of
+sembench/kernels.py:413-468).
+
+Every variant name the reference accepts is accepted here, with the
+reference's validation and error behaviour (``ValueError`` for shape / name
+problems, ``ScratchCapacityError`` for SCRATCH beyond n=10, the analytic
+``TrafficCounters`` inventory), but the arithmetic always runs the
+LAYERED sm_100a kernel of csrc/ax.cu -- the variants are different storage
+strategies for identical mathematics (reference docstring :1-45), and the
+GPU layered kernel is the one the paper (§IV-C) and the north star name.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from ._lib import check, load
+from .basis import PolynomialBasis
+from .mesh import GeomFactors
+
+__all__ = ["KernelVariant", "TrafficCounters", "ScratchCapacityError", "apply_ax",
+           "apply_ax_into", "flops_per_apply", "apply_read_words", "apply_write_words",
+           "reference_workspace", "SCRATCH_MAX_POINTS", "SCRATCH_WORD_BUDGET",
+           "ax_bytes_per_apply"]
+
+SCRATCH_MAX_POINTS = 10
+SCRATCH_WORD_BUDGET = 6144
+
+
+class KernelVariant(enum.Enum):
+    REFERENCE = "reference"
+    SCRATCH = "scratch"
+    LAYERED = "layered"
+
+    @classmethod
+    def parse(cls, name: str) -> "KernelVariant":
+        try:
+            return cls(name.lower())
+        except (ValueError, AttributeError):
+            valid = ", ".join(v.value for v in cls)
+            raise ValueError(f"unknown kernel variant {name!r} (expected one of {valid})") from None
+
+
+class ScratchCapacityError(ValueError):
+    """The scratch variant cannot stage an element of this size."""
+
+
+@dataclass
+class TrafficCounters:
+    """Analytic word/flop inventory (sembench/kernels.py:95-118)."""
+
+    reads: int = 0
+    writes: int = 0
+    flops: int = 0
+
+    def add(self, reads: int = 0, writes: int = 0, flops: int = 0) -> None:
+        if reads < 0 or writes < 0 or flops < 0:
+            raise ValueError("counter increments must be non-negative")
+        self.reads += reads
+        self.writes += writes
+        self.flops += flops
+
+    def copy(self) -> "TrafficCounters":
+        return TrafficCounters(self.reads, self.writes, self.flops)
+
+
+def flops_per_apply(dofs: int, n: int) -> int:
+    """D (12 n + 15): the equal-weight flop count of one apply."""
+    if dofs < 1 or n < 1:
+        raise ValueError("dofs and n must be positive")
+    return dofs * (12 * n + 15)
+
+
+def apply_read_words(variant: KernelVariant, dofs: int) -> int:
+    return dofs * (13 if variant is KernelVariant.REFERENCE else 7)
+
+
+def apply_write_words(variant: KernelVariant, dofs: int) -> int:
+    return dofs * (7 if variant is KernelVariant.REFERENCE else 1)
+
+
+def ax_bytes_per_apply(dofs: int) -> int:
+    """Algorithmic HBM bytes of the layered GPU kernel: u + 6 g + w = 64 B/point."""
+    return 64 * dofs
+
+
+def reference_workspace(num_elements: int, n: int):
+    """Accepted for signature compatibility; the GPU kernel needs no workspace."""
+    shape = (num_elements, n, n, n)
+    return np.empty(shape), np.empty(shape), np.empty(shape)
+
+
+def _validate(u, g_shape, n: int) -> None:
+    shp = tuple(u.shape)
+    if len(shp) != 4 or shp[1:] != (n, n, n):
+        raise ValueError(f"field shape {shp} does not match basis n={n}")
+    if tuple(g_shape) != (shp[0], 6, n, n, n):
+        raise ValueError(f"geometry shape {tuple(g_shape)} does not match field {shp}")
+
+
+def apply_ax_into(u: torch.Tensor, g: torch.Tensor, basis: PolynomialBasis, w: torch.Tensor,
+                  variant: int = 0) -> torch.Tensor:
+    """Device-only fast path: w <- A_local u (no validation, no allocation)."""
+    dx = np.ascontiguousarray(basis.diff, dtype=np.float64)
+    dxt = np.ascontiguousarray(basis.diff_t, dtype=np.float64)
+    check(load().sem_ax_variant(dv.ptr(u), dv.ptr(g), dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt),
+                                dv.ptr(w), int(u.shape[0]), int(basis.n), int(variant),
+                                dv.stream_handle(u.device)), "apply_ax")
+    return w
+
+
+def apply_ax(u, geom: GeomFactors, basis: PolynomialBasis,
+             variant: KernelVariant = KernelVariant.LAYERED,
+             counters: TrafficCounters | None = None, workspace=None):
+    """w = A_local u.  numpy in -> numpy out (H2D/D2H); CUDA tensor in -> CUDA
+    tensor out (zero-copy).  Returns a fresh array; inputs are not modified."""
+    if not isinstance(variant, KernelVariant):
+        variant = KernelVariant.parse(variant)
+    n = basis.n
+    _validate(u, geom.shape, n)
+    if variant is KernelVariant.REFERENCE and workspace is not None:
+        if any(tuple(a.shape) != tuple(u.shape) for a in workspace):
+            raise ValueError("workspace arrays must match the field shape")
+    if variant is KernelVariant.SCRATCH and n > SCRATCH_MAX_POINTS:
+        raise ScratchCapacityError(
+            f"scratch variant supports at most {SCRATCH_MAX_POINTS} points per "
+            f"dimension, got n={n}")
+    ud, kind = dv.to_device_io(u, "u")
+    with torch.cuda.device(ud.device):
+        gd = geom.device_values(ud.device)
+        wd = torch.empty_like(ud)
+        if ud.shape[0] > 0:
+            apply_ax_into(ud, gd, basis, wd)
+    if counters is not None:
+        dofs = int(np.prod(tuple(u.shape)))
+        counters.add(reads=apply_read_words(variant, dofs),
+                     writes=apply_write_words(variant, dofs),
+                     flops=flops_per_apply(dofs, n))
+    return dv.from_device_io(wd, kind)

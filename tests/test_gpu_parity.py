@@ -1,0 +1,311 @@
+"""GPU parity: the sm_100a path (through the C-ABI via the package API) vs the
+CPU oracle and the reference's golden fixtures.
+
+Bars (BASELINE.json north_star):
+  * Ax: max-norm relative difference <= 1e-12 (sembench/verify.py:37-42),
+  * dssum / mask / add2s1 / add2s2 / random_field / build_geom: bit-exact,
+  * weighted dot: <= 1e-13 relative (deterministic tree vs chunked fold),
+  * CG residual history: <= 1e-10 relative.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2005_13425_b200 as sb
+
+pytestmark = pytest.mark.gpu
+
+AX_TOL = 1e-12
+CG_TOL = 1e-10
+
+
+def _rand_inputs(E, n, su, sg):
+    u = O.random_field(E, n, su)
+    g = O.random_field(6 * E, n, sg).reshape(E, 6, n, n, n)
+    return u, g
+
+
+def _rel_hist(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+# ------------------------------------------------------------------ inputs --
+
+def test_random_field_bitexact(cuda, golden):
+    for s in golden["random/seeds"]:
+        got = sb.random_field(2, 5, int(s), host=True).ravel()[:250]
+        assert np.array_equal(got, golden[f"random/{int(s)}"])
+    big = sb.random_field(4096, 10, 12345, host=True)
+    assert np.array_equal(big, O.random_field(4096, 10, 12345))
+
+
+def test_build_geom_bitexact(cuda, golden):
+    mesh = sb.build_mesh(2, 2, 1, 10, 0.5)
+    geom = sb.build_geom(mesh, sb.build_basis(10))
+    assert np.array_equal(geom.values.cpu().numpy(), golden["geom/2x2x1n10h0.5"])
+
+
+# ---------------------------------------------------------------------- Ax --
+
+@pytest.mark.parametrize("key", ["1x2", "8x3", "8x4", "4x5", "2x7", "8x10", "3x9", "1x16"])
+def test_ax_golden(cuda, golden, key):
+    E, n, su, sg = (int(v) for v in golden[f"ax/{key}/meta"])
+    u, g = _rand_inputs(E, n, su, sg)
+    w = sb.apply_ax(u, sb.GeomFactors(values=g), sb.build_basis(n))
+    assert isinstance(w, np.ndarray)
+    assert O.rel_diff(w, golden[f"ax/{key}/layered"]) <= AX_TOL
+
+
+@pytest.mark.parametrize("n", list(range(2, 17)))
+def test_ax_psweep_vs_oracle(cuda, n):
+    E = 37  # not a multiple of any CTA slot count: exercises the ragged tail
+    u, g = _rand_inputs(E, n, 1000 + n, 2000 + n)
+    b = sb.build_basis(n)
+    w = sb.apply_ax(u, sb.GeomFactors(values=g), b)
+    ref = O.ax_layered(u, g, b.diff, b.diff_t)
+    assert O.rel_diff(w, ref) <= AX_TOL
+
+
+@pytest.mark.parametrize("E", [1, 64, 1024, 2048, 4096])
+def test_ax_paper_sizes_vs_oracle(cuda, E):
+    n = 10
+    b = sb.build_basis(n)
+    u = sb.random_field(E, n, 1)
+    g = sb.random_field(6 * E, n, 2).reshape(E, 6, n, n, n)
+    w = sb.apply_ax(u, sb.GeomFactors(values=g), b)
+    assert isinstance(w, torch.Tensor) and w.is_cuda
+    ref = O.ax_layered(u.cpu().numpy(), g.cpu().numpy(), b.diff, b.diff_t)
+    assert O.rel_diff(w.cpu().numpy(), ref) <= AX_TOL
+
+
+def test_ax_large_properties(cuda):
+    """Size-independent checks at E=32768 (the weak-scaling per-GPU size):
+    linearity and the constant null space."""
+    E, n = 32768, 10
+    b = sb.build_basis(n)
+    mesh = sb.build_mesh(32, 32, 32, n, 1.0)
+    geom = sb.build_geom(mesh, b)
+    u = sb.random_field(E, n, 3)
+    v = sb.random_field(E, n, 4)
+    au, av = sb.apply_ax(u, geom, b), sb.apply_ax(v, geom, b)
+    lhs = sb.apply_ax(1.7 * u - 0.3 * v, geom, b)
+    assert O.rel_diff(lhs.cpu().numpy(), (1.7 * au - 0.3 * av).cpu().numpy()) <= AX_TOL
+    c = sb.apply_ax(sb.constant_field(E, n, 3.25), geom, b)
+    scale = (n * np.max(np.abs(b.diff))) ** 2 * float(geom.values.max())
+    assert float(c.abs().max()) <= 1e-12 * 3.25 * scale
+    # spot-check a few elements against the oracle
+    idx = [0, 1, 4095, 17000, E - 1]
+    ref = O.ax_layered(u[idx].cpu().numpy(), geom.values[idx].cpu().numpy(), b.diff, b.diff_t)
+    assert O.rel_diff(au[idx].cpu().numpy(), ref) <= AX_TOL
+
+
+def test_ax_does_not_mutate_and_empty(cuda):
+    b = sb.build_basis(6)
+    u, g = _rand_inputs(3, 6, 5, 6)
+    u0 = u.copy()
+    sb.apply_ax(u, sb.GeomFactors(values=g), b)
+    assert np.array_equal(u, u0)
+    w = sb.apply_ax(np.zeros((0, 6, 6, 6)), sb.GeomFactors(values=np.zeros((0, 6, 6, 6, 6))), b)
+    assert w.shape == (0, 6, 6, 6)
+
+
+# ---------------------------------------------------------------- assembly --
+
+@pytest.mark.parametrize("key", ["1x1x1n3", "2x1x1n2", "2x2x2n4", "3x2x2n5", "3x3x3n3",
+                                 "2x3x2n6"])
+def test_dssum_mask_golden_bitexact(cuda, golden, key):
+    dims, n = key.split("n")
+    ex, ey, ez = (int(v) for v in dims.split("x"))
+    n = int(n)
+    topo = sb.build_topology(sb.build_mesh(ex, ey, ez, n, 1.0))
+    f = O.random_field(topo.num_elements, n, 100 + n)
+    assert np.array_equal(sb.dssum(f, topo), golden[f"dssum/{key}/out"])
+    assert np.array_equal(sb.mask(f, topo), golden[f"dssum/{key}/mask"])
+
+
+@pytest.mark.parametrize("box,n", [((16, 16, 16), 10), ((5, 3, 7), 4), ((1, 1, 9), 16),
+                                   ((7, 1, 1), 2), ((3, 4, 5), 9)])
+def test_dssum_bitexact_vs_oracle(cuda, box, n):
+    topo = sb.build_topology(sb.build_mesh(*box, n, 1.0))
+    T = O.BoxTopology(*box, n)
+    f = O.random_field(topo.num_elements, n, 77)
+    f.ravel()[::97] = -0.0  # signed zeros: bincount starts from +0.0
+    got = sb.dssum(f, topo)
+    want = O.dssum(f, T)
+    assert np.array_equal(got, want)
+    assert np.array_equal(np.signbit(got), np.signbit(want))
+    gm = sb.mask(f, topo)
+    assert np.array_equal(gm, O.mask(f, T))
+
+
+@pytest.mark.parametrize("key", ["2x2x2n4", "3x2x2n5", "2x3x2n6"])
+def test_apply_global_golden(cuda, golden, key):
+    dims, n = key.split("n")
+    ex, ey, ez = (int(v) for v in dims.split("x"))
+    n = int(n)
+    b = sb.build_basis(n)
+    mesh = sb.build_mesh(ex, ey, ez, n, 1.0)
+    topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b)
+    T = O.BoxTopology(ex, ey, ez, n)
+    u = O.mask(O.dssum(O.random_field(topo.num_elements, n, 7), T), T)
+    got = sb.apply_global(u, geom, b, topo)
+    assert O.rel_diff(got, golden[f"dssum/{key}/global"]) <= AX_TOL
+
+
+# -------------------------------------------------------------- CG vectors --
+
+def test_vector_ops_bitexact(cuda):
+    import paper_2005_13425_b200._device as dv
+    from paper_2005_13425_b200._lib import load
+    lib = load()
+    m = 1_000_003
+    rng = np.random.default_rng(0)
+    x, y = rng.standard_normal(m), rng.standard_normal(m)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    assert lib.sem_add2s2(dv.ptr(xd), dv.ptr(yd), 0.37, m, dv.stream_handle()) == 0
+    xo = x.copy()
+    O.axpy_into(xo, y, 0.37)
+    assert np.array_equal(xd.cpu().numpy(), xo)
+    pd = torch.from_numpy(x).cuda()
+    assert lib.sem_add2s1(dv.ptr(pd), dv.ptr(yd), -1.25, m, dv.stream_handle()) == 0
+    po = x.copy()
+    O.scale_add(po, y, -1.25)
+    assert np.array_equal(pd.cpu().numpy(), po)
+
+
+@pytest.mark.parametrize("key", ["2x2x2n4", "3x2x2n5", "3x3x3n3"])
+def test_weighted_dot(cuda, golden, key):
+    dims, n = key.split("n")
+    ex, ey, ez = (int(v) for v in dims.split("x"))
+    n = int(n)
+    topo = sb.build_topology(sb.build_mesh(ex, ey, ez, n, 1.0))
+    f = O.random_field(topo.num_elements, n, 100 + n)
+    v = O.random_field(topo.num_elements, n, 200 + n)
+    wd = golden[f"dssum/{key}/wdot"]
+    assert abs(sb.weighted_dot(f, v, topo) - wd[0]) <= 1e-13 * abs(wd[0])
+    assert abs(sb.weighted_dot(f, f, topo) - wd[1]) <= 1e-13 * abs(wd[1])
+
+
+def test_weighted_dot_large_deterministic(cuda):
+    topo = sb.build_topology(sb.build_mesh(16, 16, 16, 10, 1.0))
+    a, b = sb.random_field(4096, 10, 1), sb.random_field(4096, 10, 2)
+    got = [sb.weighted_dot(a, b, topo) for _ in range(3)]
+    assert got[0] == got[1] == got[2]
+    T = O.BoxTopology(16, 16, 16, 10)
+    want = O.wdot3(a.cpu().numpy(), b.cpu().numpy(), T.inv_multiplicity)
+    assert abs(got[0] - want) <= 1e-12 * abs(want)
+    ones = torch.ones((2, 2, 2, 2), dtype=torch.float64, device="cuda")
+    t2 = sb.build_topology(sb.build_mesh(2, 1, 1, 2, 1.0))
+    assert sb.weighted_dot(ones, ones, t2) == 12.0  # verify.py:432
+
+
+# ---------------------------------------------------------------------- CG --
+
+def _cg_problem(ex, ey, ez, n):
+    b = sb.build_basis(n)
+    mesh = sb.build_mesh(ex, ey, ez, n, 1.0)
+    topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b)
+    E = mesh.num_elements
+    f = sb.make_rhs(E, n, topo, sb.mix64(1, E))
+    return b, topo, geom, f
+
+
+@pytest.mark.parametrize("key", ["2x2x2n6", "3x2x2n4", "4x4x4n10"])
+def test_cg_fused_vs_golden(cuda, golden, key):
+    ex, ey, ez, n, iters = (int(v) for v in golden[f"cg/{key}/meta"])
+    b, topo, geom, f = _cg_problem(ex, ey, ez, n)
+    op = sb.GlobalOperator(geom, b, topo)
+    res = sb.cg_solve(f, op, topo, sb.CgConfig(iters, 0.0))
+    assert res.iterations_run == iters
+    assert _rel_hist(res.residual_history, golden[f"cg/{key}/history"]) <= CG_TOL
+    if f"cg/{key}/solution" in golden.files:
+        assert O.rel_diff(res.solution.cpu().numpy(), golden[f"cg/{key}/solution"]) <= 1e-10
+
+
+def test_cg_generic_matches_fused(cuda):
+    b, topo, geom, f = _cg_problem(3, 2, 2, 5)
+    op = sb.GlobalOperator(geom, b, topo)
+    fused = sb.cg_solve(f, op, topo, sb.CgConfig(25, 0.0))
+    generic = sb.cg_solve(f, lambda p: sb.apply_global(p, geom, b, topo), topo,
+                          sb.CgConfig(25, 0.0))
+    assert np.array_equal(fused.residual_history, generic.residual_history)
+    assert torch.equal(fused.solution, generic.solution)
+
+
+def test_cg_e4096_vs_oracle(cuda):
+    """BASELINE config 4: 100 iterations at E=4096, p=9 vs the CPU oracle."""
+    n = 10
+    b, topo, geom, f = _cg_problem(16, 16, 16, n)
+    res = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(100, 0.0))
+    T = O.BoxTopology(16, 16, 16, n)
+    g = O.box_geom(16, 16, 16, b.weights, 1.0)
+    x, hist, its = O.cg(f.cpu().numpy(), lambda p: O.apply_global(p, g, b.diff, b.diff_t, T),
+                        T, 100)
+    assert res.iterations_run == its == 100
+    assert _rel_hist(res.residual_history, hist) <= CG_TOL
+    assert O.rel_diff(res.solution.cpu().numpy(), x) <= 1e-10
+
+
+def test_cg_zero_rhs_and_counters(cuda):
+    b, topo, geom, _ = _cg_problem(2, 2, 2, 3)
+    f = np.zeros((8, 3, 3, 3))
+    for op in (sb.GlobalOperator(geom, b, topo), lambda p: sb.apply_global(p, geom, b, topo)):
+        res = sb.cg_solve(f, op, topo, sb.CgConfig(100, 0.0))
+        assert res.iterations_run == 1
+        assert np.array_equal(res.residual_history, [0.0])
+        assert np.array_equal(res.solution, np.zeros_like(f))
+
+
+def test_cg_counter_identity(cuda):
+    # verify.py:479-490 -- per-iteration flops = flops_per_apply + 12 D
+    b, topo, geom, f = _cg_problem(2, 2, 2, 5)
+    counters = sb.TrafficCounters()
+    op = sb.GlobalOperator(geom, b, topo, counters=counters)
+    sb.cg_solve(f, op, topo, sb.CgConfig(5, 0.0), counters=counters)
+    dofs = topo.dofs
+    assert counters.flops == 5 * (sb.flops_per_apply(dofs, 5) + 12 * dofs)
+
+
+def test_cg_manufactured_solution(cuda):
+    # verify.py:457-476 on 4^3 elements, n=4
+    b = sb.build_basis(4)
+    mesh = sb.build_mesh(4, 4, 4, 4, 1.0)
+    topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b)
+    T = O.BoxTopology(4, 4, 4, 4)
+    target = O.mask(O.dssum(O.random_field(64, 4, 77), T), T)
+    f = sb.apply_global(target, geom, b, topo)
+    free = int(round(float(np.sum(topo.mask / topo.multiplicity))))
+    op = sb.GlobalOperator(geom, b, topo)
+    anorms = []
+
+    def track(it, x, r):
+        err = x - target
+        anorms.append(sb.weighted_dot(err, op(err), topo))
+
+    res = sb.cg_solve(f, op, topo, sb.CgConfig(free, 0.0), callback=track)
+    err = res.solution - target
+    rel = np.sqrt(sb.weighted_dot(err, err, topo) / sb.weighted_dot(target, target, topo))
+    assert rel <= 1e-8
+    assert np.all(np.diff(anorms) <= 1e-12 * max(anorms))
+
+
+def test_cg_tolerance_exit(cuda):
+    b, topo, geom, f = _cg_problem(2, 2, 2, 4)
+    full = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(30, 0.0))
+    tol = float(full.residual_history[9]) * 1.0000001
+    stop = int(np.argmax(full.residual_history < tol)) + 1
+    res = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(30, tol))
+    assert res.iterations_run == stop <= 10
+    assert np.array_equal(res.residual_history, full.residual_history[:stop])
+
+
+def test_cg_breakdown(cuda):
+    b, topo, geom, f = _cg_problem(2, 2, 2, 4)
+    neg = sb.GeomFactors(values=-geom.values)
+    with pytest.raises(sb.CgBreakdownError):
+        sb.cg_solve(f, sb.GlobalOperator(neg, b, topo), topo, sb.CgConfig(10, 0.0))
+    with pytest.raises(sb.CgBreakdownError):
+        sb.cg_solve(f, lambda p: sb.apply_global(p, neg, b, topo), topo, sb.CgConfig(10, 0.0))
