@@ -22,6 +22,7 @@
 // Arithmetic differs from the reference only by FMA contraction and
 // association (tolerance 1e-12 max-norm relative, sembench/verify.py:37-42).
 #include "sem_common.cuh"
+#include "ax_pencil.cuh"
 
 namespace sem {
 
@@ -264,13 +265,77 @@ static int launch_ax(const double* u, const double* g, const double* dx, double*
     return 0;
 }
 
+template <int N, int SLOTS, int MINB, bool PERSIST>
+static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
+                         int64_t E, cudaStream_t stream)
+{
+    using C = PencilCfg<N>;
+    constexpr int THREADS = ((SLOTS * C::NN + 31) / 32) * 32;
+    constexpr size_t SMEM = sizeof(double) * (size_t)SLOTS * C::SLOT_DOUBLES;
+    static_assert(SMEM * MINB <= 227 * 1024, "pencil kernel shared memory");
+    DParamP<N> D;
+    for (int c = 0; c < 6; ++c)
+        for (int t = 0; t < N * N; ++t) D.d[c][t] = dx[t];
+    if (E == 0) return 0;
+    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST>;
+    static bool configured = false;  // per template instance
+    if (!configured) {
+        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)SMEM);
+        if (err != cudaSuccess) return fail_cuda(err, "sem_ax: cudaFuncSetAttribute");
+        configured = true;
+    }
+    const int64_t nbatches = (E + SLOTS - 1) / SLOTS;
+    int64_t grid = nbatches;
+    if (PERSIST) {
+        const int64_t cap = (int64_t)sm_count() * MINB;
+        grid = nbatches < cap ? nbatches : cap;
+    }
+    kern<<<(unsigned)grid, THREADS, SMEM, stream>>>(u, g, w, E, D);
+    SEM_CHECK_LAUNCH("sem_ax (pencil) launch");
+    return 0;
+}
+
+template <int N, int SLOTS, int MINB, bool PERSIST>
+static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
+                      cudaStream_t stream)
+{
+    if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 &&
+                  sizeof(double) * SLOTS * PencilCfg<N>::SLOT_DOUBLES * MINB <= 227 * 1024)
+        return launch_pencil<N, SLOTS, MINB, PERSIST>(u, g, dx, w, E, stream);
+    else
+        return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false>(u, g, dx, w, E, stream);
+}
+
+// variant 0: default (pencil kernel, PencilCfg slots, one batch per CTA);
+// 1: per-point layered kernel (first B200 version, kept for ablation);
+// 2..7: pencil tuning points (slots / CTAs per SM / persistent).
+template <int N>
+static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
+                int variant, cudaStream_t stream)
+{
+    constexpr int S = PencilCfg<N>::SLOTS;
+    switch (variant) {
+        case 0: return try_pencil<N, S, 1, false>(u, g, dx, w, E, stream);
+        case 1: return launch_ax<N>(u, g, dx, w, E, stream);
+        case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
+        case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
+        case 4: return try_pencil<N, S / 2, 2, false>(u, g, dx, w, E, stream);
+        case 5: return try_pencil<N, S + 1, 1, false>(u, g, dx, w, E, stream);
+        case 6: return try_pencil<N, (S + 2) / 3, 3, false>(u, g, dx, w, E, stream);
+        case 7: return try_pencil<N, S - 1, 1, false>(u, g, dx, w, E, stream);
+        default:
+            set_error("sem_ax: unknown variant %d", variant);
+            return SEM_E_INVALID;
+    }
+}
+
 int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
                 int n, int variant, cudaStream_t stream)
 {
-    (void)variant;
     switch (n) {
 #define SEM_AX_CASE(NV) \
-    case NV: return launch_ax<NV>(u, g, dx, w, E, stream);
+    case NV: return ax_n<NV>(u, g, dx, w, E, variant, stream);
         SEM_AX_CASE(2) SEM_AX_CASE(3) SEM_AX_CASE(4) SEM_AX_CASE(5) SEM_AX_CASE(6)
         SEM_AX_CASE(7) SEM_AX_CASE(8) SEM_AX_CASE(9) SEM_AX_CASE(10) SEM_AX_CASE(11)
         SEM_AX_CASE(12) SEM_AX_CASE(13) SEM_AX_CASE(14) SEM_AX_CASE(15) SEM_AX_CASE(16)
@@ -305,5 +370,5 @@ extern "C" int sem_ax(const double* u, const double* g, const double* dx,
 
 extern "C" int sem_ax_num_variants(int32_t n)
 {
-    return (n >= 2 && n <= 16) ? 1 : 0;
+    return (n >= 2 && n <= 16) ? 8 : 0;
 }

@@ -1,0 +1,270 @@
+// "Pencil" Ax kernel: the layered algorithm restructured so that every
+// contraction is a register-resident GEMV over a whole N-pencil whose D
+// entries are compile-time constant-bank operands.
+//
+// Why (measured, profiles/r01_ax_layered_ncu.txt): in the per-point layered
+// kernel each thread re-reads a u row / column (N values) from shared memory
+// for every point it owns, and shared-memory wavefronts count REQUESTED
+// bytes (a broadcast LDS.128 still costs 4 wavefronts), so the data path
+// moved ~450 B/point and capped the kernel near 30% of the HBM roofline.
+// Here a thread that loads an N-pencil produces N outputs from it (N^2
+// FMAs), so each contraction costs one shared load + one store per point:
+// ~17 shared accesses (~136 B) per point in total.
+//
+// Per element (one "slot" = N^2 threads), one CTA = SLOTS elements:
+//   S3  k-pencil (i,j): u column from HBM (prefetched a batch ahead),
+//       wt = D u_col (regs), column -> U (smem)                    | sync
+//   S1  i-pencil (j,k): U row -> wr = D row -> A
+//   S2  j-pencil (i,k): U col -> ws = D col -> B                    | sync
+//   S4  k-pencil: per layer k, metric (g from HBM, prefetched one layer
+//       ahead): ur -> A, us -> B, ut scattered into Wt = D^T ut    | sync
+//   S5  i-pencil: A row -> D^T -> A ;  S6 j-pencil: B col -> D^T -> B | sync
+//   S7  k-pencil: w = A + B + Wt -> HBM (coalesced)
+// The three pencil families are the same threads with different index
+// maps, chosen so consecutive threads touch consecutive addresses.  Layer
+// strides of U/B are padded (stride == N mod 16 doubles) so the strided
+// j-pencil accesses are bank-conflict free.
+#pragma once
+#include "sem_common.cuh"
+
+namespace sem {
+
+template <int N>
+struct PencilCfg {
+    static constexpr int NN = N * N;
+    static constexpr int NNN = N * N * N;
+    // layer strides in doubles
+    static constexpr int LSA = NN;                                  // row-friendly
+    static constexpr int LSB = NN + (((N - NN) % 16) + 16) % 16;    // == N (mod 16)
+    static constexpr int LSU = LSB;
+    static constexpr int SLOT_DOUBLES = N * (LSU + LSA + LSB);
+    static constexpr int SLOTS = (N <= 4)  ? (512 / NN)
+                               : (N <= 6)  ? (576 / NN)
+                               : (N <= 8)  ? 8
+                               : (N == 9)  ? 7
+                               : (N == 10) ? 6
+                               : (N <= 12) ? 4
+                               : (N <= 14) ? 2
+                               : 2;
+    static constexpr int THREADS = ((SLOTS * NN + 31) / 32) * 32;
+    static constexpr size_t SMEM = sizeof(double) * (size_t)SLOTS * SLOT_DOUBLES;
+    static constexpr bool VEC = (N % 2) == 0;
+};
+
+// One private copy of D per contraction stage: with a single copy the
+// compiler common-subexpressions the constant loads across stages and keeps
+// all N^2 values live in registers (spills); distinct copies keep each
+// stage's uniform constant loads local to the stage.  6 x N^2 x 8 B fits the
+// (CUDA >= 12.1) 32 KB kernel-parameter space.
+constexpr int kStS3 = 0, kStS1 = 1, kStS2 = 2, kStS4 = 3, kStS5 = 4, kStS6 = 5;
+
+template <int N>
+struct DParamP {
+    double d[6][N * N];
+};
+
+template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST>
+__global__ void __launch_bounds__(THREADS, MINB)
+ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
+                 double* __restrict__ w, int64_t num_elements, const DParamP<N> D)
+{
+    using C = PencilCfg<N>;
+    constexpr int NN = C::NN, NNN = C::NNN, LSU = C::LSU, LSA = C::LSA, LSB = C::LSB;
+    extern __shared__ __align__(16) double smem[];
+
+    const int tid = threadIdx.x;
+    const int slot = tid / NN;
+    const int p = tid - slot * NN;
+    const bool lane_ok = slot < SLOTS;
+    const int sl = lane_ok ? slot : 0;
+    double* U = smem + (size_t)sl * C::SLOT_DOUBLES;
+    double* A = U + N * LSU;
+    double* B = A + N * LSA;
+
+    // index maps of the three pencil families (see header comment)
+    const int kp_i = p % N, kp_j = p / N;          // k-pencil (i,j): p = j*N + i
+    const int ip_j = p % N, ip_k = p / N;          // i-pencil (j,k): p = k*N + j
+    const int jp_i = p % N, jp_k = p / N;          // j-pencil (i,k): p = k*N + i
+
+    const int64_t nbatches = (num_elements + SLOTS - 1) / SLOTS;
+    int64_t batch = blockIdx.x;
+    // PERSIST: grid-stride over batches with the next batch's u prefetched;
+    // otherwise one batch per CTA (D constants are not loop-invariant, so
+    // the compiler keeps them in uniform registers only around their use).
+
+    double ucol[N];
+    auto load_ucol = [&](int64_t b) {
+        const int64_t e = b * SLOTS + slot;
+        const bool ok = lane_ok && b < nbatches && e < num_elements;
+        const double* src = u + (ok ? e : 0) * NNN + kp_j * N + kp_i;
+#pragma unroll
+        for (int k = 0; k < N; ++k) ucol[k] = ok ? __ldg(src + k * NN) : 0.0;
+    };
+    load_ucol(batch);
+
+    for (; batch < nbatches; batch += (PERSIST ? gridDim.x : nbatches)) {
+        const int64_t e = batch * SLOTS + slot;
+        const bool active = lane_ok && e < num_elements;
+        const double* ge = g + (active ? e : 0) * (6 * NNN) + p;  // k-pencil point (i,j)
+
+        // ---- S3: k-pencil -- stage u, wt = D u_col -------------------------
+        double wt[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            if (lane_ok) U[k * LSU + p] = ucol[k];
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < N; ++l) s = fma(D.d[kStS3][k * N + l], ucol[l], s);
+            wt[k] = s;
+        }
+        // metric of layer 0, in flight during S1/S2
+        double gn[6];
+#pragma unroll
+        for (int m = 0; m < 6; ++m) gn[m] = active ? __ldg(ge + m * NNN) : 0.0;
+        __syncthreads();
+
+        // ---- S1: i-pencil (j,k): wr[i] = sum_l D[i][l] U[k][j][l] ----------
+        if (lane_ok) {
+            double row[N];
+            const double* src = U + ip_k * LSU + ip_j * N;
+            if (C::VEC) {
+#pragma unroll
+                for (int q = 0; q < N / 2; ++q) {
+                    const double2 v = reinterpret_cast<const double2*>(src)[q];
+                    row[2 * q] = v.x;
+                    row[2 * q + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int l = 0; l < N; ++l) row[l] = src[l];
+            }
+            double out[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int l = 0; l < N; ++l) s = fma(D.d[kStS1][i * N + l], row[l], s);
+                out[i] = s;
+            }
+            double* dst = A + ip_k * LSA + ip_j * N;
+            if (C::VEC) {
+#pragma unroll
+                for (int q = 0; q < N / 2; ++q)
+                    reinterpret_cast<double2*>(dst)[q] = make_double2(out[2 * q], out[2 * q + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < N; ++i) dst[i] = out[i];
+            }
+        }
+        // ---- S2: j-pencil (i,k): ws[j] = sum_l D[j][l] U[k][l][i] ----------
+        if (lane_ok) {
+            double col[N];
+            const double* src = U + jp_k * LSU + jp_i;
+#pragma unroll
+            for (int l = 0; l < N; ++l) col[l] = src[l * N];
+            double* dst = B + jp_k * LSB + jp_i;
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                double s = 0.0;
+#pragma unroll
+                for (int l = 0; l < N; ++l) s = fma(D.d[kStS2][j * N + l], col[l], s);
+                dst[j * N] = s;
+            }
+        }
+        __syncthreads();
+
+        // ---- S4: k-pencil metric per layer; ut scattered into Wt ----------
+        double Wt[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) Wt[k] = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            double gc[6];
+#pragma unroll
+            for (int m = 0; m < 6; ++m) gc[m] = gn[m];
+            if (k + 1 < N) {
+#pragma unroll
+                for (int m = 0; m < 6; ++m)
+                    gn[m] = active ? __ldg(ge + m * NNN + (k + 1) * NN) : 0.0;
+            }
+            if (lane_ok) {
+                const double a = A[k * LSA + p];
+                const double b = B[k * LSB + p];
+                const double t = wt[k];
+                const double ur = fma(gc[2], t, fma(gc[1], b, gc[0] * a));
+                const double us = fma(gc[4], t, fma(gc[3], b, gc[1] * a));
+                const double ut = fma(gc[5], t, fma(gc[4], b, gc[2] * a));
+                A[k * LSA + p] = ur;
+                B[k * LSB + p] = us;
+#pragma unroll
+                for (int kk = 0; kk < N; ++kk) Wt[kk] = fma(D.d[kStS4][k * N + kk], ut, Wt[kk]);
+            }
+        }
+        __syncthreads();
+
+        // ---- S5: i-pencil: A row <- D^T A row ------------------------------
+        if (lane_ok) {
+            double row[N];
+            double* rp = A + ip_k * LSA + ip_j * N;
+            if (C::VEC) {
+#pragma unroll
+                for (int q = 0; q < N / 2; ++q) {
+                    const double2 v = reinterpret_cast<const double2*>(rp)[q];
+                    row[2 * q] = v.x;
+                    row[2 * q + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int l = 0; l < N; ++l) row[l] = rp[l];
+            }
+            double out[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int l = 0; l < N; ++l) s = fma(D.d[kStS5][l * N + i], row[l], s);
+                out[i] = s;
+            }
+            if (C::VEC) {
+#pragma unroll
+                for (int q = 0; q < N / 2; ++q)
+                    reinterpret_cast<double2*>(rp)[q] = make_double2(out[2 * q], out[2 * q + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < N; ++i) rp[i] = out[i];
+            }
+        }
+        // ---- S6: j-pencil: B col <- D^T B col ------------------------------
+        if (lane_ok) {
+            double col[N];
+            double* cp = B + jp_k * LSB + jp_i;
+#pragma unroll
+            for (int l = 0; l < N; ++l) col[l] = cp[l * N];
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                double s = 0.0;
+#pragma unroll
+                for (int l = 0; l < N; ++l) s = fma(D.d[kStS6][l * N + j], col[l], s);
+                cp[j * N] = s;
+            }
+        }
+        // next batch's u columns: in flight across the barrier and S7
+        if (PERSIST) load_ucol(batch + gridDim.x);
+        __syncthreads();
+
+        // ---- S7: k-pencil: w = A + B + Wt ----------------------------------
+        if (active) {
+            double* we = w + e * NNN + p;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                const double v = (A[k * LSA + p] + B[k * LSB + p]) + Wt[k];
+                __stcs(we + k * NN, v);
+            }
+        }
+        // (no barrier needed: the next S3 writes only U, last read before the
+        //  second barrier of this iteration; A/B are next written after S3's
+        //  barrier)
+    }
+}
+
+}  // namespace sem

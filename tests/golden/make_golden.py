@@ -113,6 +113,13 @@ def main() -> int:
 
         res = sb.cg_solve(f, op, topo, sb.CgConfig(iters, 0.0))
         key = f"cg/{dims[0]}x{dims[1]}x{dims[2]}n{n}"
+        # the reference's OWN sensitivity to reassociation: LAYERED vs
+        # REFERENCE-variant Ax inside the same CG (bounds any faithful port)
+        alt = sb.cg_solve(f, lambda v, geom=geom, basis=basis, topo=topo:
+                          sb.apply_global(v, geom, basis, topo, "reference"),
+                          topo, sb.CgConfig(iters, 0.0))
+        h0, h1 = res.residual_history, alt.residual_history
+        d[key + "/variant_spread"] = np.array([np.max(np.abs(h1 - h0) / np.abs(h0))])
         d[key + "/meta"] = np.array([dims[0], dims[1], dims[2], n, iters], dtype=np.int64)
         d[key + "/history"] = res.residual_history
         if E * n ** 3 <= 20000:

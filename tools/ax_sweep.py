@@ -1,0 +1,85 @@
+#!/usr/bin/env python
+"""Tuning sweep: time every sem_ax variant for a set of n / E (CUDA events,
+two rotating input sets larger than L2), check each against the oracle on a
+few elements, print one JSON line per (n, E, variant)."""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle as O  # noqa: E402
+import paper_2005_13425_b200 as sb  # noqa: E402
+from paper_2005_13425_b200._lib import load  # noqa: E402
+from paper_2005_13425_b200.kernels import apply_ax_into  # noqa: E402
+from paper_2005_13425_b200.perf import measured_peaks  # noqa: E402
+
+
+def time_variant(sets, basis, variant, reps):
+    for i in range(3):
+        u, g, w = sets[i % len(sets)]
+        apply_ax_into(u, g, basis, w, variant)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(reps):
+        u, g, w = sets[i % len(sets)]
+        apply_ax_into(u, g, basis, w, variant)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", default="10")
+    ap.add_argument("--E", default="4096")
+    ap.add_argument("--variants", default="all")
+    ap.add_argument("--reps", type=int, default=200)
+    args = ap.parse_args()
+    hbm = float(measured_peaks(ROOT)["hbm_gbs"])
+    lib = load()
+    for n in [int(x) for x in args.n.split(",")]:
+        basis = sb.build_basis(n)
+        nv = lib.sem_ax_num_variants(n)
+        variants = range(nv) if args.variants == "all" else [int(v) for v in args.variants.split(",")]
+        for E in [int(x) for x in args.E.split(",")]:
+            per_set = E * n ** 3 * 64
+            nsets = max(2, int(np.ceil(3 * 126e6 / per_set)))
+            nsets = min(nsets, 8)
+            sets = []
+            for s in range(nsets):
+                u = sb.random_field(E, n, 1 + s)
+                g = sb.random_field(6 * E, n, 100 + s).reshape(E, 6, n, n, n)
+                sets.append((u, g, torch.empty_like(u)))
+            idx = sorted({0, 1, E // 2, E - 1})
+            ref = O.ax_layered(sets[0][0][idx].cpu().numpy(), sets[0][1][idx].cpu().numpy(),
+                               basis.diff, basis.diff_t)
+            for v in variants:
+                try:
+                    ms = time_variant(sets, basis, v, args.reps)
+                except Exception as exc:  # noqa: BLE001
+                    print(json.dumps({"n": n, "E": E, "variant": v, "error": str(exc)}))
+                    continue
+                u, g, w = sets[0]
+                apply_ax_into(u, g, basis, w, v)
+                err = O.rel_diff(w[idx].cpu().numpy(), ref)
+                gbs = E * n ** 3 * 64 / (ms * 1e-3) / 1e9
+                print(json.dumps({"n": n, "E": E, "variant": v, "us": round(ms * 1e3, 2),
+                                  "gflops": round(E * n ** 3 * (12 * n + 15) / (ms * 1e-3) / 1e9, 1),
+                                  "gbs": round(gbs, 1), "frac": round(gbs / hbm, 4),
+                                  "rel_err": err}), flush=True)
+            del sets
+            torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
