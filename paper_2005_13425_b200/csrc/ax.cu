@@ -265,7 +265,7 @@ static int launch_ax(const double* u, const double* g, const double* dx, double*
     return 0;
 }
 
-template <int N, int SLOTS, int MINB, bool PERSIST>
+template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false>
 static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
                          int64_t E, cudaStream_t stream)
 {
@@ -277,7 +277,7 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     for (int c = 0; c < 6; ++c)
         for (int t = 0; t < N * N; ++t) D.d[c][t] = dx[t];
     if (E == 0) return 0;
-    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST>;
+    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF>;
     static bool configured = false;  // per template instance
     if (!configured) {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -286,44 +286,59 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
         configured = true;
     }
     const int64_t nbatches = (E + SLOTS - 1) / SLOTS;
-    int64_t grid = nbatches;
-    if (PERSIST) {
-        const int64_t cap = (int64_t)sm_count() * MINB;
-        grid = nbatches < cap ? nbatches : cap;
-    }
-    kern<<<(unsigned)grid, THREADS, SMEM, stream>>>(u, g, w, E, D);
+    const int64_t resident = (int64_t)sm_count() * MINB;
+    const int64_t grid = PERSIST ? (nbatches < resident ? nbatches : resident) : nbatches;
+    // prefetch distance: the batch that replaces this one on its SM
+    const int64_t pf = (nbatches > resident) ? resident * SLOTS : 0;
+    kern<<<(unsigned)grid, THREADS, SMEM, stream>>>(u, g, w, E, D, pf);
     SEM_CHECK_LAUNCH("sem_ax (pencil) launch");
     return 0;
 }
 
-template <int N, int SLOTS, int MINB, bool PERSIST>
+template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false>
 static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
                       cudaStream_t stream)
 {
     if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 &&
                   sizeof(double) * SLOTS * PencilCfg<N>::SLOT_DOUBLES * MINB <= 227 * 1024)
-        return launch_pencil<N, SLOTS, MINB, PERSIST>(u, g, dx, w, E, stream);
+        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF>(u, g, dx, w, E, stream);
     else
         return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false>(u, g, dx, w, E, stream);
 }
 
-// variant 0: default (pencil kernel, PencilCfg slots, one batch per CTA);
+// variant 0: the tuned default for this n (kDefaultVariant);
 // 1: per-point layered kernel (first B200 version, kept for ablation);
-// 2..7: pencil tuning points (slots / CTAs per SM / persistent).
+// 2..19: pencil tuning points <elements per CTA, CTAs per SM, metric
+// prefetch depth, persistent, L2 bulk prefetch>.
+// Default tuning point per n (tools/ax_sweep.py on B200, E=4096; see
+// profiles/r01_ax_sweep.txt): index = n, value = variant id below.
+constexpr int kDefaultVariant[17] = {0, 0, 8, 7, 12, 7, 15, 15, 16, 13, 15, 9, 5, 8, 7, 17, 3};
+
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
                 int variant, cudaStream_t stream)
 {
     constexpr int S = PencilCfg<N>::SLOTS;
+    if (variant == 0) variant = kDefaultVariant[N];
     switch (variant) {
-        case 0: return try_pencil<N, S, 1, false>(u, g, dx, w, E, stream);
+        case 19: return try_pencil<N, S, 1, false>(u, g, dx, w, E, stream);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
-        case 4: return try_pencil<N, S / 2, 2, false>(u, g, dx, w, E, stream);
-        case 5: return try_pencil<N, S + 1, 1, false>(u, g, dx, w, E, stream);
+        case 4: return try_pencil<N, (S + 1) / 2, 2, false, 2>(u, g, dx, w, E, stream);
+        case 5: return try_pencil<N, (S + 1) / 2, 2, false, 3>(u, g, dx, w, E, stream);
         case 6: return try_pencil<N, (S + 2) / 3, 3, false>(u, g, dx, w, E, stream);
-        case 7: return try_pencil<N, S - 1, 1, false>(u, g, dx, w, E, stream);
+        case 7: return try_pencil<N, (S + 2) / 3, 3, false, 2>(u, g, dx, w, E, stream);
+        case 8: return try_pencil<N, (S + 2) / 3, 3, false, 3>(u, g, dx, w, E, stream);
+        case 9: return try_pencil<N, 1, 6, false, 2>(u, g, dx, w, E, stream);
+        case 10: return try_pencil<N, (S + 2) / 3, 3, false, 1, true>(u, g, dx, w, E, stream);
+        case 11: return try_pencil<N, S + 1, 1, false, 2>(u, g, dx, w, E, stream);
+        case 12: return try_pencil<N, 1, 7, false, 1>(u, g, dx, w, E, stream);
+        case 13: return try_pencil<N, 1, 7, false, 2>(u, g, dx, w, E, stream);
+        case 14: return try_pencil<N, 1, 7, false, 3>(u, g, dx, w, E, stream);
+        case 15: return try_pencil<N, 1, 5, false, 3>(u, g, dx, w, E, stream);
+        case 16: return try_pencil<N, 1, 6, false, 3>(u, g, dx, w, E, stream);
+        case 17: return try_pencil<N, (S + 1) / 2, 2, false, 4>(u, g, dx, w, E, stream);
         default:
             set_error("sem_ax: unknown variant %d", variant);
             return SEM_E_INVALID;
@@ -370,5 +385,5 @@ extern "C" int sem_ax(const double* u, const double* g, const double* dx,
 
 extern "C" int sem_ax_num_variants(int32_t n)
 {
-    return (n >= 2 && n <= 16) ? 8 : 0;
+    return (n >= 2 && n <= 16) ? 20 : 0;
 }

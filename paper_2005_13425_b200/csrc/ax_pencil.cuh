@@ -63,10 +63,28 @@ struct DParamP {
     double d[6][N * N];
 };
 
-template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST>
+// Bulk L2 prefetch (sm_90+ cp.async.bulk.prefetch.L2): one instruction
+// pulls a whole element's u or g block from HBM into L2, so the demand
+// loads of a later CTA hit L2 instead of paying DRAM latency.  Sizes and
+// addresses are rounded to the 16-byte granularity the instruction needs
+// and clamped to the array.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* base, int64_t lo, int64_t hi,
+                                                 int64_t limit)
+{
+    lo &= ~int64_t(15);
+    hi = (hi + 15) & ~int64_t(15);
+    if (hi > (limit & ~int64_t(15))) hi = limit & ~int64_t(15);
+    if (hi <= lo) return;
+    const char* p = static_cast<const char*>(base) + lo;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)(hi - lo))
+                 : "memory");
+}
+
+template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
-                 double* __restrict__ w, int64_t num_elements, const DParamP<N> D)
+                 double* __restrict__ w, int64_t num_elements, const DParamP<N> D,
+                 int64_t pf_elems)
 {
     using C = PencilCfg<N>;
     constexpr int NN = C::NN, NNN = C::NNN, LSU = C::LSU, LSA = C::LSA, LSB = C::LSB;
@@ -106,6 +124,20 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         const int64_t e = batch * SLOTS + slot;
         const bool active = lane_ok && e < num_elements;
         const double* ge = g + (active ? e : 0) * (6 * NNN) + p;  // k-pencil point (i,j)
+        // metric of layers 0..PD-1: issued first, in flight during S3/S1/S2
+        double gq[PD][6];
+#pragma unroll
+        for (int d = 0; d < PD; ++d)
+#pragma unroll
+            for (int m = 0; m < 6; ++m)
+                gq[d][m] = (active && d < N) ? __ldg(ge + m * NNN + d * NN) : 0.0;
+        // warm L2 with the element this slot will process pf_elems later
+        if (L2PF && pf_elems > 0 && lane_ok && p == 0 && e + pf_elems < num_elements) {
+            const int64_t en = e + pf_elems;
+            prefetch_l2_bulk(u, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);
+            prefetch_l2_bulk(g, en * 6 * NNN * 8, (en + 1) * 6 * NNN * 8,
+                             num_elements * 6 * NNN * 8);
+        }
 
         // ---- S3: k-pencil -- stage u, wt = D u_col -------------------------
         double wt[N];
@@ -117,10 +149,6 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             for (int l = 0; l < N; ++l) s = fma(D.d[kStS3][k * N + l], ucol[l], s);
             wt[k] = s;
         }
-        // metric of layer 0, in flight during S1/S2
-        double gn[6];
-#pragma unroll
-        for (int m = 0; m < 6; ++m) gn[m] = active ? __ldg(ge + m * NNN) : 0.0;
         __syncthreads();
 
         // ---- S1: i-pencil (j,k): wr[i] = sum_l D[i][l] U[k][j][l] ----------
@@ -179,13 +207,14 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         for (int k = 0; k < N; ++k) Wt[k] = 0.0;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
+            // register ring: consume layer k, refill the slot with layer k+PD
             double gc[6];
 #pragma unroll
-            for (int m = 0; m < 6; ++m) gc[m] = gn[m];
-            if (k + 1 < N) {
+            for (int m = 0; m < 6; ++m) gc[m] = gq[k % PD][m];
+            if (k + PD < N) {
 #pragma unroll
                 for (int m = 0; m < 6; ++m)
-                    gn[m] = active ? __ldg(ge + m * NNN + (k + 1) * NN) : 0.0;
+                    gq[k % PD][m] = active ? __ldg(ge + m * NNN + (k + PD) * NN) : 0.0;
             }
             if (lane_ok) {
                 const double a = A[k * LSA + p];
