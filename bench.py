@@ -307,7 +307,7 @@ def run_ours(args, rank, world, local_rank):
                          "gflops_roofline": hbm * (12 * n + 15) / 64.0},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * E * n ** 3,
                     "d2h_bytes_per_step": 8 * E * n ** 3,
-                    "path": "apply_ax(pinned CPU tensor u, geom resident) -> CPU tensor w",
+                    "path": "apply_ax(pinned CPU tensor u, geom resident) -> pinned CPU tensor w via sem_ax_host (chunked H2D/Ax/D2H overlap)",
                     "ms_per_step": e2e_s * 1e3},
             "gpu_launches": args.steps,
             "clocks": clocks.summary(),

@@ -21,6 +21,8 @@
 //
 // Arithmetic differs from the reference only by FMA contraction and
 // association (tolerance 1e-12 max-norm relative, sembench/verify.py:37-42).
+#include <stdlib.h>
+
 #include "sem_common.cuh"
 #include "ax_pencil.cuh"
 
@@ -265,6 +267,8 @@ static int launch_ax(const double* u, const double* g, const double* dx, double*
     return 0;
 }
 
+constexpr int kAxCarveout = -1;
+
 template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false>
 static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
                          int64_t E, cudaStream_t stream)
@@ -283,6 +287,15 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)SMEM);
         if (err != cudaSuccess) return fail_cuda(err, "sem_ax: cudaFuncSetAttribute");
+        // smem/L1 split: the streaming u/g loads need L1 capacity for their
+        // in-flight lines, so the carveout is a tuning knob (measured in
+        // profiles/; SEM_AX_CARVEOUT overrides, -1 = driver default)
+        int carve = kAxCarveout;
+        if (const char* env = getenv("SEM_AX_CARVEOUT")) carve = atoi(env);
+        if (carve >= 0) {
+            err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+            if (err != cudaSuccess) return fail_cuda(err, "sem_ax: carveout");
+        }
         configured = true;
     }
     const int64_t nbatches = (E + SLOTS - 1) / SLOTS;

@@ -27,31 +27,41 @@ int bind_stream_device(cudaStream_t stream)
     // The legacy/per-thread default streams belong to the current device.
     if (stream == nullptr || stream == cudaStreamLegacy || stream == cudaStreamPerThread)
         return 0;
+    // Fast path: same stream as the previous call on this thread -> its
+    // device is already current (no runtime call, so this is also safe
+    // inside CUDA-graph capture).
     static thread_local cudaStream_t last_stream = nullptr;
     static thread_local int last_device = -1;
-    int dev = last_device;
-    if (stream != last_stream || dev < 0) {
-        cudaError_t err = cudaStreamGetDevice(stream, &dev);
-        if (err != cudaSuccess) return fail_cuda(err, "cudaStreamGetDevice");
-        last_stream = stream;
-        last_device = dev;
-    }
+    if (stream == last_stream && last_device >= 0) return 0;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+        return 0;  // capturing: the capturing thread already has the right device
+    int dev = -1;
+    cudaError_t err = cudaStreamGetDevice(stream, &dev);
+    if (err != cudaSuccess) return fail_cuda(err, "cudaStreamGetDevice");
     int cur = -1;
-    cudaError_t err = cudaGetDevice(&cur);
+    err = cudaGetDevice(&cur);
     if (err != cudaSuccess) return fail_cuda(err, "cudaGetDevice");
     if (cur != dev) {
         err = cudaSetDevice(dev);
         if (err != cudaSuccess) return fail_cuda(err, "cudaSetDevice");
     }
+    last_stream = stream;
+    last_device = dev;
     return 0;
 }
 
 int sm_count()
 {
-    int dev = 0, n = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMsB200;
+    // cached per device: attribute queries are not needed on the launch path
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kNumSMsB200;
+    if (cache[dev] > 0) return cache[dev];
+    int n = 0;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
         return kNumSMsB200;
+    cache[dev] = n;
     return n;
 }
 

@@ -12,6 +12,7 @@ GPU layered kernel is the one the paper (§IV-C) and the north star name.
 
 from __future__ import annotations
 
+import ctypes
 import enum
 from dataclasses import dataclass
 
@@ -130,15 +131,67 @@ def apply_ax(u, geom: GeomFactors, basis: PolynomialBasis,
         raise ScratchCapacityError(
             f"scratch variant supports at most {SCRATCH_MAX_POINTS} points per "
             f"dimension, got n={n}")
-    ud, kind = dv.to_device_io(u, "u")
-    with torch.cuda.device(ud.device):
-        gd = geom.device_values(ud.device)
-        wd = torch.empty_like(ud)
-        if ud.shape[0] > 0:
-            apply_ax_into(ud, gd, basis, wd)
+    kind = dv.io_kind(u)
+    if kind == "device":
+        with torch.cuda.device(u.device):
+            ud = dv.as_device_f64(u, u.device, "u")
+            gd = geom.device_values(ud.device)
+            wd = torch.empty_like(ud)
+            if ud.shape[0] > 0:
+                apply_ax_into(ud, gd, basis, wd)
+        result = wd
+    else:
+        result = _apply_ax_host(u, kind, geom, basis)
     if counters is not None:
         dofs = int(np.prod(tuple(u.shape)))
         counters.add(reads=apply_read_words(variant, dofs),
                      writes=apply_write_words(variant, dofs),
                      flops=flops_per_apply(dofs, n))
-    return dv.from_device_io(wd, kind)
+    return result
+
+
+# elements per streamed chunk for host-buffer calls (~2 MB of u)
+HOST_CHUNK_BYTES = 2 << 20
+_host_scratch: dict = {}
+
+
+def _host_device_scratch(dev: torch.device, numel: int):
+    key = dev.index
+    buf = _host_scratch.get(key)
+    if buf is None or buf.shape[1] < numel:
+        buf = torch.empty((2, numel), dtype=torch.float64, device=dev)
+        _host_scratch[key] = buf
+    return buf[0, :numel], buf[1, :numel]
+
+
+def _apply_ax_host(u, kind: str, geom: GeomFactors, basis: PolynomialBasis):
+    """Host arrays in/out through sem_ax_host: chunked H2D / Ax / D2H on
+    library-owned copy streams (csrc/host.cu).  Pageable inputs are first
+    staged into pinned memory; the result is a pinned CPU tensor (numpy view
+    for numpy callers)."""
+    dev = dv.current_device()
+    shape = tuple(u.shape)
+    E, n = shape[0], basis.n
+    if E == 0:
+        out = torch.empty(shape, dtype=torch.float64)
+        return out.numpy() if kind == "numpy" else out
+    if kind == "numpy":
+        src = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64))
+    else:
+        src = u.to(torch.float64).contiguous()
+    if not src.is_pinned():
+        src = src.pin_memory()
+    out = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+    dx = np.ascontiguousarray(basis.diff, dtype=np.float64)
+    dxt = np.ascontiguousarray(basis.diff_t, dtype=np.float64)
+    with torch.cuda.device(dev):
+        gd = geom.device_values(dev)
+        ud, wd = _host_device_scratch(dev, E * n ** 3)
+        stream = torch.cuda.current_stream(dev)
+        chunk = max(1, HOST_CHUNK_BYTES // (8 * n ** 3))
+        check(load().sem_ax_host(ctypes.c_void_p(src.data_ptr()), dv.ptr(gd),
+                                 dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt),
+                                 ctypes.c_void_p(out.data_ptr()), E, n, dv.ptr(ud), dv.ptr(wd),
+                                 chunk, ctypes.c_void_p(stream.cuda_stream)), "apply_ax")
+        stream.synchronize()
+    return out.numpy() if kind == "numpy" else out
