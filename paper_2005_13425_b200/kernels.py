@@ -150,8 +150,9 @@ def apply_ax(u, geom: GeomFactors, basis: PolynomialBasis,
     return result
 
 
-# elements per streamed chunk for host-buffer calls (~2 MB of u)
-HOST_CHUNK_BYTES = 2 << 20
+# elements per streamed chunk for host-buffer calls: 8 MB of u was the
+# best point of the chunk sweep on B200 + PCIe Gen5 (tools/e2e_probe.py)
+HOST_CHUNK_BYTES = 8 << 20
 _host_scratch: dict = {}
 
 
@@ -179,9 +180,12 @@ def _apply_ax_host(u, kind: str, geom: GeomFactors, basis: PolynomialBasis):
         src = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64))
     else:
         src = u.to(torch.float64).contiguous()
-    if not src.is_pinned():
-        src = src.pin_memory()
-    out = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+    staged = None
+    if not src.is_pinned():  # stage pageable input through a recycled pinned block
+        staged = dv.pinned_pool.scratch(src.numel() * 8)
+        src = staged.view(torch.float64)[:src.numel()].view(shape).copy_(src)
+    out_np = dv.pinned_pool.array(shape)
+    out = torch.from_numpy(out_np)
     dx = np.ascontiguousarray(basis.diff, dtype=np.float64)
     dxt = np.ascontiguousarray(basis.diff_t, dtype=np.float64)
     with torch.cuda.device(dev):
@@ -194,4 +198,6 @@ def _apply_ax_host(u, kind: str, geom: GeomFactors, basis: PolynomialBasis):
                                  ctypes.c_void_p(out.data_ptr()), E, n, dv.ptr(ud), dv.ptr(wd),
                                  chunk, ctypes.c_void_p(stream.cuda_stream)), "apply_ax")
         stream.synchronize()
-    return out.numpy() if kind == "numpy" else out
+    if staged is not None:
+        dv.pinned_pool.release(staged)
+    return out_np if kind == "numpy" else out
