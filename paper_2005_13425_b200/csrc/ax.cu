@@ -324,8 +324,8 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 // 2..19: pencil tuning points <elements per CTA, CTAs per SM, metric
 // prefetch depth, persistent, L2 bulk prefetch>.
 // Default tuning point per n (tools/ax_sweep.py on B200, E=4096; see
-// profiles/r01_ax_sweep.txt): index = n, value = variant id below.
-constexpr int kDefaultVariant[17] = {0, 0, 8, 7, 12, 7, 15, 15, 16, 13, 15, 9, 5, 8, 7, 17, 3};
+// profiles/r01_ax_sweep.txt, CUDA-graph timed): index = n, value = variant id.
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 19, 16, 15, 16, 9, 13, 15, 9, 5, 8, 7, 17, 3};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
