@@ -28,7 +28,10 @@ dssum_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t
     constexpr int NN = N * N, NNN = N * N * N;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
         const ElemCoord c = elem_coord(e, b);
-        for (int r = threadIdx.x; r < NNN; r += kBoxThreads) {
+        #pragma unroll
+        for (int t_ = 0; t_ < (NNN + kBoxThreads - 1) / kBoxThreads; ++t_) {
+            const int r = threadIdx.x + t_ * kBoxThreads;
+            if (r >= NNN) break;
             const int k = r / NN, j = (r / N) % N, i = r % N;
             double s = gather_sum<N>(f, c, i, j, k, b);
             if (MASK) s = mul_rn(s, mask_val<N>(c, i, j, k, b));
@@ -44,7 +47,10 @@ mask_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t 
     constexpr int NN = N * N, NNN = N * N * N;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
         const ElemCoord c = elem_coord(e, b);
-        for (int r = threadIdx.x; r < NNN; r += kBoxThreads) {
+        #pragma unroll
+        for (int t_ = 0; t_ < (NNN + kBoxThreads - 1) / kBoxThreads; ++t_) {
+            const int r = threadIdx.x + t_ * kBoxThreads;
+            if (r >= NNN) break;
             const int k = r / NN, j = (r / N) % N, i = r % N;
             out[e * NNN + r] = mul_rn(__ldg(f + e * NNN + r), mask_val<N>(c, i, j, k, b));
         }
@@ -53,7 +59,7 @@ mask_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t 
 
 static unsigned box_grid(int64_t E)
 {
-    const int64_t cap = 8LL * sm_count();
+    const int64_t cap = 16LL * sm_count();
     return (unsigned)(E < cap ? (E > 0 ? E : 1) : cap);
 }
 

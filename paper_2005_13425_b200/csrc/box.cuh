@@ -95,24 +95,24 @@ __device__ __forceinline__ double gather_sum(const double* __restrict__ f, const
     const AxisCopies ax = axis_copies<N>(c.ix, i, b.ex);
     const AxisCopies ay = axis_copies<N>(c.iy, j, b.ey);
     const AxisCopies az = axis_copies<N>(c.iz, k, b.ez);
+    // issue every copy's load first (predicated), then add in the
+    // reference order: z-choice outer, y middle, x inner = ascending e
+    double v[8];
+    bool ok[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int zc = q >> 2, yc = (q >> 1) & 1, xc = q & 1;
+        ok[q] = zc < az.cnt && yc < ay.cnt && xc < ax.cnt;
+        const int ez_ = zc ? az.e1 : az.e0, kk = zc ? az.l1 : az.l0;
+        const int ey_ = yc ? ay.e1 : ay.e0, jj = yc ? ay.l1 : ay.l0;
+        const int ex_ = xc ? ax.e1 : ax.e0, ii = xc ? ax.l1 : ax.l0;
+        const int64_t e2 = ((int64_t)ez_ * b.ey + ey_) * b.ex + ex_;
+        v[q] = ok[q] ? __ldg(f + e2 * NNN + (kk * N + jj) * N + ii) : 0.0;
+    }
     double s = 0.0;
 #pragma unroll
-    for (int zc = 0; zc < 2; ++zc) {
-        if (zc >= az.cnt) break;
-        const int ez_ = zc ? az.e1 : az.e0, kk = zc ? az.l1 : az.l0;
-#pragma unroll
-        for (int yc = 0; yc < 2; ++yc) {
-            if (yc >= ay.cnt) break;
-            const int ey_ = yc ? ay.e1 : ay.e0, jj = yc ? ay.l1 : ay.l0;
-#pragma unroll
-            for (int xc = 0; xc < 2; ++xc) {
-                if (xc >= ax.cnt) break;
-                const int ex_ = xc ? ax.e1 : ax.e0, ii = xc ? ax.l1 : ax.l0;
-                const int64_t e2 = ((int64_t)ez_ * b.ey + ey_) * b.ex + ex_;
-                s = add_rn(s, __ldg(f + e2 * NNN + (kk * N + jj) * N + ii));
-            }
-        }
-    }
+    for (int q = 0; q < 8; ++q)
+        if (ok[q]) s = add_rn(s, v[q]);
     return s;
 }
 

@@ -77,7 +77,10 @@ glsc3_box_kernel(const double* __restrict__ a, const double* __restrict__ b, int
     double acc = 0.0;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
         const ElemCoord c = elem_coord(e, bx);
-        for (int q = threadIdx.x; q < NNN; q += kReduceThreads) {
+        #pragma unroll
+        for (int t_ = 0; t_ < (NNN + kReduceThreads - 1) / kReduceThreads; ++t_) {
+            const int q = threadIdx.x + t_ * kReduceThreads;
+            if (q >= NNN) break;
             const int k = q / NN, j = (q / N) % N, i = q % N;
             const int64_t idx = e * NNN + q;
             acc += mul_rn(mul_rn(__ldg(a + idx), __ldg(b + idx)), inv_mult<N>(c, i, j, k, bx));
@@ -99,7 +102,10 @@ cg_init_kernel(const double* __restrict__ f, double* __restrict__ x, double* __r
     double acc = 0.0;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
         const ElemCoord c = elem_coord(e, bx);
-        for (int q = threadIdx.x; q < NNN; q += kReduceThreads) {
+        #pragma unroll
+        for (int t_ = 0; t_ < (NNN + kReduceThreads - 1) / kReduceThreads; ++t_) {
+            const int q = threadIdx.x + t_ * kReduceThreads;
+            if (q >= NNN) break;
             const int k = q / NN, j = (q / N) % N, i = q % N;
             const int64_t idx = e * NNN + q;
             const double rv = mul_rn(__ldg(f + idx), mask_val<N>(c, i, j, k, bx));
@@ -160,7 +166,10 @@ cg_assemble_kernel(const double* __restrict__ w, double* __restrict__ w2,
     double acc = 0.0;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
         const ElemCoord c = elem_coord(e, bx);
-        for (int q = threadIdx.x; q < NNN; q += kReduceThreads) {
+        #pragma unroll
+        for (int t_ = 0; t_ < (NNN + kReduceThreads - 1) / kReduceThreads; ++t_) {
+            const int q = threadIdx.x + t_ * kReduceThreads;
+            if (q >= NNN) break;
             const int k = q / NN, j = (q / N) % N, i = q % N;
             const int64_t idx = e * NNN + q;
             const double v = mul_rn(gather_sum<N>(w, c, i, j, k, bx), mask_val<N>(c, i, j, k, bx));
@@ -194,7 +203,10 @@ cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* _
     double acc = 0.0;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
         const ElemCoord c = elem_coord(e, bx);
-        for (int q = threadIdx.x; q < NNN; q += kReduceThreads) {
+        #pragma unroll
+        for (int t_ = 0; t_ < (NNN + kReduceThreads - 1) / kReduceThreads; ++t_) {
+            const int q = threadIdx.x + t_ * kReduceThreads;
+            if (q >= NNN) break;
             const int k = q / NN, j = (q / N) % N, i = q % N;
             const int64_t idx = e * NNN + q;
             x[idx] = add_rn(x[idx], mul_rn(alpha, __ldg(p + idx)));

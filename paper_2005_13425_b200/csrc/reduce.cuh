@@ -12,7 +12,7 @@
 
 namespace sem {
 
-constexpr int kReduceBlocks = 296;   // 2 x 148; a constant so the tree is fixed
+constexpr int kReduceBlocks = 1184;  // 8 x 148; a constant so the tree is fixed
 constexpr int kReduceThreads = 256;
 constexpr int kMaxReductions = 4;    // independent accumulators per kernel
 
