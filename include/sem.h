@@ -122,6 +122,7 @@ typedef struct sem_cg_state {
                           2 breakdown <p,Ap> <= 0, 3 tolerance reached */
     int32_t breakdown_it;
     int32_t pad_;
+    double local_sum;  /* multi-GPU: this rank's partial of the last reduction */
 } sem_cg_state;
 
 /* Initialise: r = mask(f), x = p = 0, rtz = <r,r>_c, state fields. */
@@ -135,6 +136,51 @@ int sem_cg_run(const double *g, const double *dx, const double *dxt, double *x,
                double *r, double *p, double *w, sem_cg_state *state, double *history,
                int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,
                void *scratch, sem_stream_t stream);
+
+/* ------------------------------------------- multi-GPU z-slab partition -- */
+/* A rank owns global element layers [gz0, gz0+ez) of an ex*ey*ez_global box
+ * (contiguous element range, e = ix + ex*(iy + ey*iz)).  Interface planes are
+ * (ey*(n-1)+1) x (ex*(n-1)+1) arrays indexed gy*(ex*(n-1)+1) + gx.
+ * Halo protocol (bit-exact with the reference's bincount order):
+ *   plane_top    : ordered in-plane sum of this slab's top-face copies, from +0.0
+ *   plane_bottom : `prefix` (the lower rank's plane_top, or NULL = +0.0)
+ *                  continued with this slab's bottom-face copies = totals   */
+int sem_slab_plane_top(const double *f, double *plane, int32_t ex, int32_t ey, int32_t ez,
+                       int32_t n, sem_stream_t stream);
+int sem_slab_plane_bottom(const double *f, const double *prefix, double *totals, int32_t ex,
+                          int32_t ey, int32_t ez, int32_t n, sem_stream_t stream);
+/* dssum on a slab: nodes on the bottom/top face shared with another rank take
+ * bottom_totals / top_totals (NULL = no neighbour), the rest are gathered
+ * locally; the mask and multiplicities use the GLOBAL lattice. */
+int sem_dssum_slab(const double *f, double *out, const double *bottom_totals,
+                   const double *top_totals, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+                   int32_t gz0, int32_t ez_global, int32_t apply_mask, sem_stream_t stream);
+int sem_mask_slab(const double *f, double *out, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+                  int32_t gz0, int32_t ez_global, sem_stream_t stream);
+/* this rank's partial of the weighted dot (global multiplicities) */
+int sem_glsc3_slab(const double *a, const double *b, int32_t ex, int32_t ey, int32_t ez,
+                   int32_t n, int32_t gz0, int32_t ez_global, double *out_dev, void *scratch,
+                   sem_stream_t stream);
+/* Distributed CG phases: each reduction leaves this rank's partial in
+ * state->local_sum; after gathering all ranks' partials (rank order) into
+ * `gathered`, sem_cg_finish(phase) combines them in rank order and performs
+ * the phase's scalar step (0: rtz after init, 1: pap -> alpha / breakdown,
+ * 2: <r,r> -> history, rtz, tolerance). */
+int sem_cg_init_slab(const double *f, double *x, double *r, double *p, sem_cg_state *state,
+                     double *history, int32_t max_iterations, double tolerance, int32_t ex,
+                     int32_t ey, int32_t ez, int32_t n, int32_t gz0, int32_t ez_global,
+                     void *scratch, sem_stream_t stream);
+int sem_cg_p(double *p, const double *r, int64_t m, sem_cg_state *state, double *history,
+             sem_stream_t stream);
+int sem_cg_assemble_slab(const double *w, double *w2, const double *p,
+                         const double *bottom_totals, const double *top_totals,
+                         sem_cg_state *state, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+                         int32_t gz0, int32_t ez_global, void *scratch, sem_stream_t stream);
+int sem_cg_update_slab(double *x, double *r, const double *p, const double *w2,
+                       sem_cg_state *state, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+                       int32_t gz0, int32_t ez_global, void *scratch, sem_stream_t stream);
+int sem_cg_finish(sem_cg_state *state, const double *gathered, int32_t nranks, int32_t phase,
+                  double *history, sem_stream_t stream);
 
 /* ------------------------------------------------------ input builders -- */
 int sem_random_field(double *out, int64_t count, uint64_t seed, sem_stream_t stream);

@@ -34,6 +34,7 @@ class sem_cg_state(ctypes.Structure):
         ("stop", ctypes.c_int32),
         ("breakdown_it", ctypes.c_int32),
         ("pad_", ctypes.c_int32),
+        ("local_sum", ctypes.c_double),
     ]
 
 
@@ -67,6 +68,21 @@ SIGNATURES = {
                                    _i32, _vp, _vp]),
     "sem_cg_run": (ctypes.c_int, [_vp, _dp, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,
                                   _i32, _i32, _vp, _vp]),
+    "sem_slab_plane_top": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    "sem_slab_plane_bottom": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    "sem_dssum_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
+                                      _i32, _vp]),
+    "sem_mask_slab": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp]),
+    "sem_glsc3_slab": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp,
+                                      _vp]),
+    "sem_cg_init_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _f64, _i32, _i32,
+                                        _i32, _i32, _i32, _i32, _vp, _vp]),
+    "sem_cg_p": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
+    "sem_cg_assemble_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,
+                                            _i32, _i32, _i32, _vp, _vp]),
+    "sem_cg_update_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
+                                          _i32, _vp, _vp]),
+    "sem_cg_finish": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
     "sem_random_field": (ctypes.c_int, [_vp, _i64, ctypes.c_uint64, _vp]),
     "sem_box_geom": (ctypes.c_int, [_vp, _i64, _i32, _dp, _f64, _vp]),
 }

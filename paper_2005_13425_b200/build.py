@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsem.so")
-SOURCES = ["common.cu", "ax.cu", "assembly.cu", "cg.cu", "fields.cu", "host.cu"]
+SOURCES = ["common.cu", "ax.cu", "assembly.cu", "cg.cu", "fields.cu", "host.cu", "slab.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

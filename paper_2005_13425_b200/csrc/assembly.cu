@@ -23,7 +23,8 @@ constexpr int kBoxThreads = 256;
 // MASK: multiply by the 0/1 mask (reference mask() is f*mask).
 template <int N, bool MASK>
 __global__ void __launch_bounds__(kBoxThreads)
-dssum_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, Box b)
+dssum_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, Box b,
+                 const double* __restrict__ bot, const double* __restrict__ top)
 {
     constexpr int NN = N * N, NNN = N * N * N;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
@@ -33,7 +34,8 @@ dssum_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t
             const int r = threadIdx.x + t_ * kBoxThreads;
             if (r >= NNN) break;
             const int k = r / NN, j = (r / N) % N, i = r % N;
-            double s = gather_sum<N>(f, c, i, j, k, b);
+            double s;
+            if (!slab_face_value<N>(c, i, j, k, b, bot, top, s)) s = gather_sum<N>(f, c, i, j, k, b);
             if (MASK) s = mul_rn(s, mask_val<N>(c, i, j, k, b));
             out[e * NNN + r] = s;
         }
@@ -65,13 +67,13 @@ static unsigned box_grid(int64_t E)
 
 template <int N>
 static int launch_dssum(const double* f, double* out, int64_t E, Box b, bool mask,
-                        cudaStream_t s)
+                        cudaStream_t s, const double* bot = nullptr, const double* top = nullptr)
 {
     if (E == 0) return 0;
     if (mask)
-        dssum_box_kernel<N, true><<<box_grid(E), kBoxThreads, 0, s>>>(f, out, E, b);
+        dssum_box_kernel<N, true><<<box_grid(E), kBoxThreads, 0, s>>>(f, out, E, b, bot, top);
     else
-        dssum_box_kernel<N, false><<<box_grid(E), kBoxThreads, 0, s>>>(f, out, E, b);
+        dssum_box_kernel<N, false><<<box_grid(E), kBoxThreads, 0, s>>>(f, out, E, b, bot, top);
     SEM_CHECK_LAUNCH("sem_dssum_box launch");
     return 0;
 }
@@ -110,6 +112,19 @@ int mask_box(const double* f, double* out, int ex, int ey, int ez, int n, cudaSt
 {
     const Box b{ex, ey, ez, 0, ez};
     const int64_t E = (int64_t)ex * ey * ez;
+    SEM_SWITCH_N(n, return launch_mask<NV>(f, out, E, b, s));
+}
+
+int dssum_slab(const double* f, double* out, const double* bot, const double* top, const Box& b,
+               int n, bool mask, cudaStream_t s)
+{
+    const int64_t E = (int64_t)b.ex * b.ey * b.ez;
+    SEM_SWITCH_N(n, return launch_dssum<NV>(f, out, E, b, mask, s, bot, top));
+}
+
+int mask_slab(const double* f, double* out, const Box& b, int n, cudaStream_t s)
+{
+    const int64_t E = (int64_t)b.ex * b.ey * b.ez;
     SEM_SWITCH_N(n, return launch_mask<NV>(f, out, E, b, s));
 }
 

@@ -116,6 +116,27 @@ __device__ __forceinline__ double gather_sum(const double* __restrict__ f, const
     return s;
 }
 
+// Multi-GPU z-slabs: the field holds global element layers [gz0, gz0+ez).
+// Nodes on a slab face shared with a neighbouring rank take their assembled
+// value from a plane of totals exchanged by the halo protocol (dist.py);
+// plane index = gy * (ex*(n-1)+1) + gx over the global x/y lattice.
+template <int N>
+__device__ __forceinline__ bool slab_face_value(const ElemCoord& c, int i, int j, int k,
+                                                const Box& b, const double* __restrict__ bot,
+                                                const double* __restrict__ top, double& v)
+{
+    const int nx = b.ex * (N - 1) + 1;
+    if (bot != nullptr && c.iz == 0 && k == 0) {
+        v = __ldg(bot + (int64_t)(c.iy * (N - 1) + j) * nx + (c.ix * (N - 1) + i));
+        return true;
+    }
+    if (top != nullptr && c.iz == b.ez - 1 && k == N - 1) {
+        v = __ldg(top + (int64_t)(c.iy * (N - 1) + j) * nx + (c.ix * (N - 1) + i));
+        return true;
+    }
+    return false;
+}
+
 // Dispatch a runtime n in [2,16] to a compile-time NV.
 #define SEM_SWITCH_N(n, ...)                                                          \
     switch (n) {                                                                      \

@@ -91,8 +91,57 @@ glsc3_box_kernel(const double* __restrict__ a, const double* __restrict__ b, int
 }
 
 // ------------------------------------------------------------ CG kernels --
+// Scalar bookkeeping of the three reductions of an iteration, shared by the
+// single-GPU kernels (total = this GPU's sum) and the multi-GPU finish kernel
+// (total = per-rank partials combined in rank order).
+constexpr int kPhaseInit = 0, kPhasePap = 1, kPhaseRr = 2;
+
+__device__ __forceinline__ void fin_init(sem_cg_state* st, double rtz)
+{
+    st->rtz = rtz;
+    st->rtz_old = 1.0;  // cg.py:146 (unused: beta = 0 on iteration 1)
+    st->pap = 0.0;
+    st->alpha = 0.0;
+    st->beta = 0.0;
+    st->it = 0;
+    st->iterations_run = 0;
+    st->stop = 0;
+    st->breakdown_it = 0;
+}
+
+__device__ __forceinline__ void fin_pap(sem_cg_state* st, double pap)
+{
+    st->pap = pap;
+    if (pap <= 0.0) {  // cg.py:164-169 breakdown
+        st->stop = 2;
+        st->breakdown_it = st->it + 1;
+    } else {
+        st->alpha = st->rtz / pap;
+    }
+}
+
+__device__ __forceinline__ void fin_rr(sem_cg_state* st, double rtr, double* history)
+{
+    const int it = st->it + 1;
+    const double rnorm = sqrt(rtr);
+    history[it - 1] = rnorm;
+    st->iterations_run = it;
+    st->rtz_old = st->rtz;
+    st->rtz = rtr;  // equals <r,r>_c at the top of the next iteration
+    st->it = it;
+    if (st->tolerance > 0.0 && rnorm < st->tolerance) st->stop = 3;
+}
+
+__device__ __forceinline__ void fin_phase(sem_cg_state* st, int phase, double total,
+                                          double* history)
+{
+    if (phase == kPhaseInit) fin_init(st, total);
+    else if (phase == kPhasePap) fin_pap(st, total);
+    else fin_rr(st, total, history);
+}
+
 // init: r = mask(f) (assembly.py:123-129), x = p = 0, rtz = <r,r>_c.
-template <int N>
+template <int N, bool DIST>
 __global__ void __launch_bounds__(kReduceThreads)
 cg_init_kernel(const double* __restrict__ f, double* __restrict__ x, double* __restrict__ r,
                double* __restrict__ p, int64_t E, Box bx, sem_cg_state* st, ReduceScratch* rs,
@@ -117,17 +166,14 @@ cg_init_kernel(const double* __restrict__ f, double* __restrict__ x, double* __r
     }
     const double vals[1] = {acc};
     reduce_publish_and_finish<1, kReduceThreads>(vals, rs, [&](const double (&t)[1]) {
-        st->rtz = t[0];
-        st->rtz_old = 1.0;  // cg.py:146 (unused: beta = 0 on iteration 1)
-        st->pap = 0.0;
-        st->alpha = 0.0;
-        st->beta = 0.0;
-        st->it = 0;
-        st->iterations_run = 0;
-        st->stop = 0;
-        st->breakdown_it = 0;
         st->max_iterations = max_iterations;
         st->tolerance = tolerance;
+        if (DIST) {
+            st->local_sum = t[0];
+            fin_init(st, 0.0);  // rtz set by sem_cg_finish once ranks are combined
+        } else {
+            fin_init(st, t[0]);
+        }
     });
 }
 
@@ -155,11 +201,12 @@ cg_p_kernel(double* __restrict__ p, const double* __restrict__ r, int64_t m, sem
 }
 
 // w2 = mask(dssum(w)) and <p, w2>_c (assembly.py:113-129 + cg.py:163-170).
-template <int N>
+template <int N, bool DIST>
 __global__ void __launch_bounds__(kReduceThreads)
 cg_assemble_kernel(const double* __restrict__ w, double* __restrict__ w2,
                    const double* __restrict__ p, int64_t E, Box bx, sem_cg_state* st,
-                   ReduceScratch* rs)
+                   ReduceScratch* rs, const double* __restrict__ bot,
+                   const double* __restrict__ top)
 {
     constexpr int NN = N * N, NNN = N * N * N;
     if (st->stop) return;
@@ -172,26 +219,23 @@ cg_assemble_kernel(const double* __restrict__ w, double* __restrict__ w2,
             if (q >= NNN) break;
             const int k = q / NN, j = (q / N) % N, i = q % N;
             const int64_t idx = e * NNN + q;
-            const double v = mul_rn(gather_sum<N>(w, c, i, j, k, bx), mask_val<N>(c, i, j, k, bx));
+            double sv;
+            if (!DIST || !slab_face_value<N>(c, i, j, k, bx, bot, top, sv))
+                sv = gather_sum<N>(w, c, i, j, k, bx);
+            const double v = mul_rn(sv, mask_val<N>(c, i, j, k, bx));
             w2[idx] = v;
             acc += mul_rn(mul_rn(__ldg(p + idx), v), inv_mult<N>(c, i, j, k, bx));
         }
     }
     const double vals[1] = {acc};
     reduce_publish_and_finish<1, kReduceThreads>(vals, rs, [&](const double (&t)[1]) {
-        const double pap = t[0];
-        st->pap = pap;
-        if (pap <= 0.0) {
-            st->stop = 2;
-            st->breakdown_it = st->it + 1;
-        } else {
-            st->alpha = st->rtz / pap;
-        }
+        if (DIST) st->local_sum = t[0];
+        else fin_pap(st, t[0]);
     });
 }
 
 // x += alpha p ; r += (-alpha) w2 ; rnorm = sqrt(<r,r>_c)  (cg.py:170-186).
-template <int N>
+template <int N, bool DIST>
 __global__ void __launch_bounds__(kReduceThreads)
 cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                  const double* __restrict__ w2, int64_t E, Box bx, sem_cg_state* st,
@@ -217,15 +261,8 @@ cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* _
     }
     const double vals[1] = {acc};
     reduce_publish_and_finish<1, kReduceThreads>(vals, rs, [&](const double (&t)[1]) {
-        const double rtr = t[0];
-        const int it = st->it + 1;
-        const double rnorm = sqrt(rtr);
-        history[it - 1] = rnorm;
-        st->iterations_run = it;
-        st->rtz_old = st->rtz;
-        st->rtz = rtr;   // equals <r,r>_c at the top of the next iteration
-        st->it = it;
-        if (st->tolerance > 0.0 && rnorm < st->tolerance) st->stop = 3;
+        if (DIST) st->local_sum = t[0];
+        else fin_rr(st, t[0], history);
     });
 }
 
@@ -239,8 +276,8 @@ static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_st
                      int64_t E, Box bx, ReduceScratch* rs, int max_it, double tol,
                      cudaStream_t s)
 {
-    cg_init_kernel<N><<<red_grid(E), kReduceThreads, 0, s>>>(f, x, r, p, E, bx, st, rs,
-                                                              max_it, tol);
+    cg_init_kernel<N, false><<<red_grid(E), kReduceThreads, 0, s>>>(f, x, r, p, E, bx, st, rs,
+                                                                     max_it, tol);
     SEM_CHECK_LAUNCH("sem_cg_init launch");
     return 0;
 }
@@ -256,10 +293,11 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
         cg_p_kernel<<<vec_grid(m), kVecThreads, 0, s>>>(p, r, m, st, history);
         SEM_CHECK_LAUNCH("cg_p_kernel");
         if (int rc = ax_dispatch(p, g, dx, w, E, N, 0, s)) return rc;
-        cg_assemble_kernel<N><<<red_grid(E), kReduceThreads, 0, s>>>(w, w2, p, E, bx, st, rs);
+        cg_assemble_kernel<N, false><<<red_grid(E), kReduceThreads, 0, s>>>(w, w2, p, E, bx, st,
+                                                                             rs, nullptr, nullptr);
         SEM_CHECK_LAUNCH("cg_assemble_kernel");
-        cg_update_kernel<N><<<red_grid(E), kReduceThreads, 0, s>>>(x, r, p, w2, E, bx, st,
-                                                                    history, rs);
+        cg_update_kernel<N, false><<<red_grid(E), kReduceThreads, 0, s>>>(x, r, p, w2, E, bx,
+                                                                           st, history, rs);
         SEM_CHECK_LAUNCH("cg_update_kernel");
     }
     return 0;
@@ -370,4 +408,158 @@ extern "C" int sem_cg_run(const double* g, const double* dx, const double* dxt, 
     double* w_asm = w + m;
     SEM_SWITCH_N(n, return cg_run_n<NV>(g, dx, x, r, p, w_local, w_asm, state, history,
                                         iterations, E, bx, rs, s));
+}
+
+// ------------------------------------------------- multi-GPU (z-slab) CG --
+// The same kernels with DIST=true: each reduction leaves this rank's partial
+// in state->local_sum; the host gathers the partials of all ranks (NCCL
+// all_gather, dist.py) and sem_cg_finish combines them in rank order and
+// runs the phase's scalar bookkeeping -- identically on every rank.
+
+namespace sem {
+
+__global__ void cg_finish_kernel(sem_cg_state* st, const double* __restrict__ gathered,
+                                 int nranks, int phase, double* history)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (phase != kPhaseInit && st->stop) return;
+    double total = 0.0;
+    for (int r = 0; r < nranks; ++r) total += gathered[r];
+    fin_phase(st, phase, total, history);
+}
+
+static Box slab_box(int ex, int ey, int ez, int gz0, int ezg) { return Box{ex, ey, ez, gz0, ezg}; }
+
+static int check_slab(int ex, int ey, int ez, int n, int gz0, int ezg, const char* who)
+{
+    if (int rc = check_box(ex, ey, ez, n, who)) return rc;
+    if (gz0 < 0 || ezg < gz0 + ez) {
+        set_error("%s: slab [%d, %d) outside the global %d element layers", who, gz0, gz0 + ez,
+                  ezg);
+        return SEM_E_INVALID;
+    }
+    return 0;
+}
+
+}  // namespace sem
+
+extern "C" int sem_cg_init_slab(const double* f, double* x, double* r, double* p,
+                                sem_cg_state* state, double* history, int32_t max_iterations,
+                                double tolerance, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+                                int32_t gz0, int32_t ez_global, void* scratch,
+                                sem_stream_t stream)
+{
+    if (int rc = check_slab(ex, ey, ez, n, gz0, ez_global, "sem_cg_init_slab")) return rc;
+    if (!f || !x || !r || !p || !state || !history || !scratch || max_iterations < 1 ||
+        tolerance < 0.0) {
+        set_error("sem_cg_init_slab: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const Box bx = slab_box(ex, ey, ez, gz0, ez_global);
+    const int64_t E = (int64_t)ex * ey * ez;
+    auto* rs = static_cast<ReduceScratch*>(scratch);
+    SEM_SWITCH_N(n, {
+        cg_init_kernel<NV, true><<<red_grid(E), kReduceThreads, 0, s>>>(
+            f, x, r, p, E, bx, state, rs, max_iterations, tolerance);
+        SEM_CHECK_LAUNCH("sem_cg_init_slab launch");
+        return 0;
+    });
+}
+
+extern "C" int sem_cg_p(double* p, const double* r, int64_t m, sem_cg_state* state,
+                        double* history, sem_stream_t stream)
+{
+    if (!p || !r || !state || !history || m < 0) {
+        set_error("sem_cg_p: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    cg_p_kernel<<<vec_grid(m), kVecThreads, 0, s>>>(p, r, m, state, history);
+    SEM_CHECK_LAUNCH("sem_cg_p launch");
+    return 0;
+}
+
+extern "C" int sem_cg_assemble_slab(const double* w, double* w2, const double* p,
+                                    const double* bottom_totals, const double* top_totals,
+                                    sem_cg_state* state, int32_t ex, int32_t ey, int32_t ez,
+                                    int32_t n, int32_t gz0, int32_t ez_global, void* scratch,
+                                    sem_stream_t stream)
+{
+    if (int rc = check_slab(ex, ey, ez, n, gz0, ez_global, "sem_cg_assemble_slab")) return rc;
+    if (!w || !w2 || !p || !state || !scratch || w == w2) {
+        set_error("sem_cg_assemble_slab: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const Box bx = slab_box(ex, ey, ez, gz0, ez_global);
+    const int64_t E = (int64_t)ex * ey * ez;
+    auto* rs = static_cast<ReduceScratch*>(scratch);
+    SEM_SWITCH_N(n, {
+        cg_assemble_kernel<NV, true><<<red_grid(E), kReduceThreads, 0, s>>>(
+            w, w2, p, E, bx, state, rs, bottom_totals, top_totals);
+        SEM_CHECK_LAUNCH("sem_cg_assemble_slab launch");
+        return 0;
+    });
+}
+
+extern "C" int sem_cg_update_slab(double* x, double* r, const double* p, const double* w2,
+                                  sem_cg_state* state, int32_t ex, int32_t ey, int32_t ez,
+                                  int32_t n, int32_t gz0, int32_t ez_global, void* scratch,
+                                  sem_stream_t stream)
+{
+    if (int rc = check_slab(ex, ey, ez, n, gz0, ez_global, "sem_cg_update_slab")) return rc;
+    if (!x || !r || !p || !w2 || !state || !scratch) {
+        set_error("sem_cg_update_slab: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const Box bx = slab_box(ex, ey, ez, gz0, ez_global);
+    const int64_t E = (int64_t)ex * ey * ez;
+    auto* rs = static_cast<ReduceScratch*>(scratch);
+    SEM_SWITCH_N(n, {
+        cg_update_kernel<NV, true><<<red_grid(E), kReduceThreads, 0, s>>>(
+            x, r, p, w2, E, bx, state, nullptr, rs);
+        SEM_CHECK_LAUNCH("sem_cg_update_slab launch");
+        return 0;
+    });
+}
+
+extern "C" int sem_cg_finish(sem_cg_state* state, const double* gathered, int32_t nranks,
+                             int32_t phase, double* history, sem_stream_t stream)
+{
+    if (!state || !gathered || nranks < 1 || phase < 0 || phase > 2 || !history) {
+        set_error("sem_cg_finish: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    cg_finish_kernel<<<1, 32, 0, s>>>(state, gathered, nranks, phase, history);
+    SEM_CHECK_LAUNCH("sem_cg_finish launch");
+    return 0;
+}
+
+extern "C" int sem_glsc3_slab(const double* a, const double* b, int32_t ex, int32_t ey,
+                              int32_t ez, int32_t n, int32_t gz0, int32_t ez_global,
+                              double* out_dev, void* scratch, sem_stream_t stream)
+{
+    if (int rc = check_slab(ex, ey, ez, n, gz0, ez_global, "sem_glsc3_slab")) return rc;
+    if (!a || !b || !out_dev || !scratch) {
+        set_error("sem_glsc3_slab: null pointer");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const Box bx = slab_box(ex, ey, ez, gz0, ez_global);
+    const int64_t E = (int64_t)ex * ey * ez;
+    auto* rs = static_cast<ReduceScratch*>(scratch);
+    SEM_SWITCH_N(n, {
+        glsc3_box_kernel<NV><<<red_grid(E), kReduceThreads, 0, s>>>(a, b, E, bx, out_dev, rs);
+        SEM_CHECK_LAUNCH("sem_glsc3_slab launch");
+        return 0;
+    });
 }

@@ -1,0 +1,308 @@
+"""Multi-GPU CG on an element-partitioned box (BASELINE config 5).
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  The
+reference's element order e = ix + ex*(iy + ey*iz) (sembench/assembly.py:
+76-79) makes contiguous element ranges z-slabs, so rank r owns global element
+layers [z0, z1) and its local fields are exactly the slice [z0*ex*ey,
+z1*ex*ey) of the global arrays.
+
+Per CG iteration (the recurrence of sembench/cg.py:148-186):
+
+    p = beta p + r                      local                      (sem_cg_p)
+    w = A_local p                       local                      (sem_ax)
+    halo, step 1: top-face partial sums  -> rank r+1               (plane_top)
+    halo, step 2: continue the prefix with own bottom-face copies
+                  -> interface totals    -> rank r-1               (plane_bottom)
+    w2 = mask(dssum(w)) with the faces taken from the totals,
+         local <p, w2>_c partial        -> all_gather -> alpha     (assemble, finish)
+    x += alpha p, r -= alpha w2, local <r, r>_c -> all_gather       (update, finish)
+
+The two-step halo reproduces the reference's bincount order bit-for-bit:
+every copy on rank r-1's side of an interface has a lower element id than
+any copy on rank r's side, so rank r-1's ordered partial IS the prefix of the
+reference's sum.  Dot products combine per-rank partials in rank order on
+every rank (deterministic, identical scalars everywhere; the early-exit
+flags therefore agree across ranks).
+
+The driver is written against two small interfaces -- ``SlabOps`` (the
+per-rank compute) and ``SlabComm`` (the exchanges) -- so the choreography is
+exercised on CPU with the gloo backend in tests/test_dist_gloo.py; the
+product implementation of ``SlabOps`` is ``CudaSlabOps`` (libsem kernels).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _device as dv
+from ._lib import check, load, sem_cg_state
+
+__all__ = ["SlabPartition", "SlabComm", "CudaSlabOps", "dist_cg_solve", "dist_dssum",
+           "halo_exchange", "DistCgResult"]
+
+
+@dataclass(frozen=True)
+class SlabPartition:
+    """Rank `rank` of `world` owns global element layers [z0, z1)."""
+
+    ex: int
+    ey: int
+    ez_global: int
+    n: int
+    world: int
+    rank: int
+
+    def __post_init__(self):
+        if not (0 <= self.rank < self.world):
+            raise ValueError(f"rank {self.rank} outside world of size {self.world}")
+        if self.ez_global < self.world:
+            raise ValueError(f"{self.ez_global} element layers cannot be split over "
+                             f"{self.world} ranks (each needs >= 1 layer)")
+
+    @staticmethod
+    def layer_range(ez_global: int, world: int, rank: int) -> tuple[int, int]:
+        base, extra = divmod(ez_global, world)
+        z0 = rank * base + min(rank, extra)
+        return z0, z0 + base + (1 if rank < extra else 0)
+
+    @property
+    def z0(self) -> int:
+        return self.layer_range(self.ez_global, self.world, self.rank)[0]
+
+    @property
+    def z1(self) -> int:
+        return self.layer_range(self.ez_global, self.world, self.rank)[1]
+
+    @property
+    def ez(self) -> int:
+        return self.z1 - self.z0
+
+    @property
+    def num_elements(self) -> int:
+        return self.ex * self.ey * self.ez
+
+    @property
+    def element_range(self) -> tuple[int, int]:
+        per = self.ex * self.ey
+        return self.z0 * per, self.z1 * per
+
+    @property
+    def lower(self):
+        return self.rank - 1 if self.z0 > 0 else None
+
+    @property
+    def upper(self):
+        return self.rank + 1 if self.z1 < self.ez_global else None
+
+    @property
+    def plane_size(self) -> int:
+        return (self.ex * (self.n - 1) + 1) * (self.ey * (self.n - 1) + 1)
+
+
+class SlabComm:
+    """The two halo exchanges and the scalar all-gather over torch.distributed.
+
+    NCCL moves device tensors directly; with gloo (CPU tests, or several
+    processes sharing one GPU) device tensors are staged through host memory.
+    """
+
+    def __init__(self, part: SlabPartition, group=None):
+        self.part = part
+        self.group = group
+        self.backend = dist.get_backend(group)
+        self.stage = self.backend != "nccl"
+
+    def _xfer(self, sends: list, recvs: list) -> None:
+        ops = []
+        staged = []
+        for t, peer in sends:
+            src = t.cpu() if (self.stage and t.is_cuda) else t
+            ops.append(dist.P2POp(dist.isend, src, peer, self.group))
+        for t, peer in recvs:
+            dst = torch.empty(t.shape, dtype=t.dtype) if (self.stage and t.is_cuda) else t
+            staged.append((t, dst))
+            ops.append(dist.P2POp(dist.irecv, dst, peer, self.group))
+        if not ops:
+            return
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        for t, dst in staged:
+            if dst is not t:
+                t.copy_(dst)
+
+    def exchange_up(self, top_partial, bottom_prefix) -> None:
+        """Send this slab's top-face partial to rank+1; receive rank-1's."""
+        p = self.part
+        self._xfer([(top_partial, p.upper)] if p.upper is not None else [],
+                   [(bottom_prefix, p.lower)] if p.lower is not None else [])
+
+    def exchange_down(self, bottom_totals, top_totals) -> None:
+        """Send the bottom interface totals to rank-1; receive rank+1's."""
+        p = self.part
+        self._xfer([(bottom_totals, p.lower)] if p.lower is not None else [],
+                   [(top_totals, p.upper)] if p.upper is not None else [])
+
+    def allgather(self, local: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        if self.stage and local.is_cuda:
+            tmp = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_gather_into_tensor(tmp, local.cpu(), group=self.group)
+            out.copy_(tmp)
+        else:
+            dist.all_gather_into_tensor(out, local, group=self.group)
+        return out
+
+
+class CudaSlabOps:
+    """Per-rank compute of the distributed CG on the GPU (csrc/cg.cu, slab.cu)."""
+
+    def __init__(self, part: SlabPartition, g_local: torch.Tensor, basis, max_iterations: int,
+                 device: torch.device):
+        self.part, self.basis, self.dev = part, basis, device
+        n = part.n
+        shape = (part.num_elements, n, n, n)
+        mk = lambda: torch.empty(shape, dtype=torch.float64, device=device)  # noqa: E731
+        self.x, self.r, self.p, self.w, self.w2 = mk(), mk(), mk(), mk(), mk()
+        self.g = g_local
+        self.history = torch.zeros(max(1, max_iterations), dtype=torch.float64, device=device)
+        self.state = torch.zeros(ctypes.sizeof(sem_cg_state), dtype=torch.uint8, device=device)
+        self.scratch = torch.zeros(int(load().sem_reduce_scratch_bytes()), dtype=torch.uint8,
+                                   device=device)
+        ps = part.plane_size
+        self.top_partial = torch.zeros(ps, dtype=torch.float64, device=device)
+        self.bottom_prefix = torch.zeros(ps, dtype=torch.float64, device=device)
+        self.bottom_totals = torch.zeros(ps, dtype=torch.float64, device=device)
+        self.top_totals = torch.zeros(ps, dtype=torch.float64, device=device)
+        self.dx = np.ascontiguousarray(basis.diff, dtype=np.float64)
+        self.dxt = np.ascontiguousarray(basis.diff_t, dtype=np.float64)
+        self.lib = load()
+        self._local = self.state.view(torch.float64)[9:10]  # sem_cg_state.local_sum
+
+    # geometry of this slab as the C-ABI expects it
+    def _slab(self):
+        p = self.part
+        return (p.ex, p.ey, p.ez, p.n, p.z0, p.ez_global)
+
+    def _s(self):
+        return dv.stream_handle(self.dev)
+
+    def init(self, f: torch.Tensor, max_iterations: int, tolerance: float) -> None:
+        check(self.lib.sem_cg_init_slab(dv.ptr(f), dv.ptr(self.x), dv.ptr(self.r), dv.ptr(self.p),
+                                        dv.ptr(self.state), dv.ptr(self.history), max_iterations,
+                                        float(tolerance), *self._slab(), dv.ptr(self.scratch),
+                                        self._s()), "dist cg init")
+
+    def local_sum(self) -> torch.Tensor:
+        return self._local
+
+    def finish(self, phase: int, gathered: torch.Tensor) -> None:
+        check(self.lib.sem_cg_finish(dv.ptr(self.state), dv.ptr(gathered), gathered.numel(),
+                                     phase, dv.ptr(self.history), self._s()), "dist cg finish")
+
+    def p_update(self) -> None:
+        check(self.lib.sem_cg_p(dv.ptr(self.p), dv.ptr(self.r), self.p.numel(),
+                                dv.ptr(self.state), dv.ptr(self.history), self._s()), "cg p")
+
+    def ax(self) -> None:
+        p = self.part
+        check(self.lib.sem_ax(dv.ptr(self.p), dv.ptr(self.g), dv.host_f64_ptr(self.dx),
+                              dv.host_f64_ptr(self.dxt), dv.ptr(self.w), p.num_elements, p.n,
+                              self._s()), "dist cg ax")
+
+    def plane_top(self, field: torch.Tensor) -> torch.Tensor:
+        p = self.part
+        check(self.lib.sem_slab_plane_top(dv.ptr(field), dv.ptr(self.top_partial), p.ex, p.ey,
+                                          p.ez, p.n, self._s()), "plane top")
+        return self.top_partial
+
+    def plane_bottom(self, field: torch.Tensor, prefix) -> torch.Tensor:
+        p = self.part
+        check(self.lib.sem_slab_plane_bottom(dv.ptr(field), dv.ptr(prefix),
+                                             dv.ptr(self.bottom_totals), p.ex, p.ey, p.ez, p.n,
+                                             self._s()), "plane bottom")
+        return self.bottom_totals
+
+    def dssum(self, field: torch.Tensor, bottom_totals, top_totals, apply_mask: bool = False):
+        """Standalone distributed dssum of `field` (faces from the halo totals)."""
+        p = self.part
+        out = torch.empty_like(field)
+        ptr = lambda t: dv.ptr(t) if t is not None else ctypes.c_void_p(0)  # noqa: E731
+        check(self.lib.sem_dssum_slab(dv.ptr(field), dv.ptr(out), ptr(bottom_totals),
+                                      ptr(top_totals), p.ex, p.ey, p.ez, p.n, p.z0, p.ez_global,
+                                      1 if apply_mask else 0, self._s()), "dist dssum")
+        return out
+
+    def assemble(self, bottom_totals, top_totals) -> None:
+        ptr = lambda t: dv.ptr(t) if t is not None else ctypes.c_void_p(0)  # noqa: E731
+        check(self.lib.sem_cg_assemble_slab(dv.ptr(self.w), dv.ptr(self.w2), dv.ptr(self.p),
+                                            ptr(bottom_totals), ptr(top_totals),
+                                            dv.ptr(self.state), *self._slab(),
+                                            dv.ptr(self.scratch), self._s()), "dist assemble")
+
+    def update(self) -> None:
+        check(self.lib.sem_cg_update_slab(dv.ptr(self.x), dv.ptr(self.r), dv.ptr(self.p),
+                                          dv.ptr(self.w2), dv.ptr(self.state), *self._slab(),
+                                          dv.ptr(self.scratch), self._s()), "dist update")
+
+    def scalar_buffer(self, world: int) -> torch.Tensor:
+        return torch.zeros(world, dtype=torch.float64, device=self.dev)
+
+    def result(self):
+        raw = self.state.cpu().numpy().tobytes()
+        st = sem_cg_state.from_buffer_copy(raw)
+        iters = int(st.iterations_run)
+        hist = self.history[:iters].cpu().numpy().copy()
+        return self.x, hist, iters, int(st.stop), float(st.pap), int(st.breakdown_it)
+
+
+def halo_exchange(ops, comm: SlabComm, field):
+    """The two-step ordered halo of one assembled field.  Returns the
+    (bottom_totals, top_totals) planes this rank needs (None = no neighbour)."""
+    part = comm.part
+    top = ops.plane_top(field) if part.upper is not None else None
+    comm.exchange_up(top, ops.bottom_prefix if part.lower is not None else None)
+    bot = ops.plane_bottom(field, ops.bottom_prefix) if part.lower is not None else None
+    comm.exchange_down(bot, ops.top_totals if part.upper is not None else None)
+    return bot, (ops.top_totals if part.upper is not None else None)
+
+
+def dist_dssum(ops, comm: SlabComm, field, apply_mask: bool = False):
+    """dssum of a slab-partitioned field, bit-identical to the global one."""
+    bot, top = halo_exchange(ops, comm, field)
+    return ops.dssum(field, bot, top, apply_mask)
+
+
+@dataclass
+class DistCgResult:
+    solution: object          # this rank's slice of the solution
+    residual_history: np.ndarray
+    iterations_run: int
+    stop: int
+
+
+def dist_cg_solve(ops, comm: SlabComm, f_local, max_iterations: int, tolerance: float = 0.0
+                  ) -> DistCgResult:
+    """Distributed CG; every rank calls this with its slab (same arguments)."""
+    part = comm.part
+    world = part.world
+    gathered = ops.scalar_buffer(world)
+    ops.init(f_local, max_iterations, tolerance)
+    ops.finish(0, comm.allgather(ops.local_sum(), gathered))
+    for _ in range(max_iterations):
+        ops.p_update()
+        ops.ax()
+        bot, top = halo_exchange(ops, comm, ops.w)
+        ops.assemble(bot, top)
+        ops.finish(1, comm.allgather(ops.local_sum(), gathered))
+        ops.update()
+        ops.finish(2, comm.allgather(ops.local_sum(), gathered))
+    x, hist, iters, stop, pap, bit = ops.result()
+    if stop == 2:
+        from .cg import CgBreakdownError
+        raise CgBreakdownError(f"<p, A p>_c = {pap:.3e} at iteration {bit}; "
+                               "operator is not SPD here")
+    return DistCgResult(solution=x, residual_history=hist, iterations_run=iters, stop=stop)

@@ -56,7 +56,7 @@ def test_invalid_arguments_rejected_without_gpu(lib):
 
 def test_state_struct_layout():
     from paper_2005_13425_b200._lib import sem_cg_state
-    assert ctypes.sizeof(sem_cg_state) == 6 * 8 + 6 * 4
+    assert ctypes.sizeof(sem_cg_state) == 7 * 8 + 6 * 4
 
 
 def test_product_never_imports_oracle():
