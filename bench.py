@@ -283,8 +283,12 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- secondary: full Nekbone CG, 100 iterations (BASELINE config 4) ----
     cg = None
-    if args.cg:
+    if args.cg and rank == 0 and world == 1:
         cg = bench_cg(sb, dev, 100)
+    # ---- secondary: weak-scaled CG, 32768 elements per GPU (BASELINE config 5) ----
+    cg_weak = None
+    if args.cg_weak:
+        cg_weak = bench_cg_weak(sb, dev, world, rank, args.cg_weak_iters)
 
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ax_ncu_summary.json")
@@ -323,6 +327,8 @@ def run_ours(args, rank, world, local_rank):
         }
         if cg is not None:
             line["cg_e4096_p9"] = cg
+        if cg_weak is not None:
+            line["cg_weak_e32768_per_gpu"] = cg_weak
         print(json.dumps(line), flush=True)
     return 0
 
@@ -358,6 +364,69 @@ def bench_cg(sb, dev, iters):
                     "timed with CUDA events incl. one host sync at the end"}
 
 
+def bench_cg_weak(sb, dev, world, rank, iters):
+    """Weak-scaled CG: E=32768 per GPU, p=9, global box factor_elements(32768*G)
+    split into z-slabs (dist.py).  G=1 runs the fused single-GPU solver."""
+    import torch
+    import torch.distributed as dist
+    from paper_2005_13425_b200 import perf
+    from paper_2005_13425_b200.dist import CudaSlabOps, SlabComm, SlabPartition, dist_cg_solve
+    n, per = N_HEAD, 32768
+    ex, ey, ez = sb.factor_elements(per * world)
+    b = sb.build_basis(n)
+    e_total = ex * ey * ez
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world == 1:
+        mesh = sb.build_mesh(ex, ey, ez, n, 1.0)
+        topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b, device=dev)
+        f = sb.make_rhs(e_total, n, topo, sb.mix64(1, e_total), device=dev)
+        op = sb.GlobalOperator(geom, b, topo)
+        ws = sb.CgWorkspace(topo, iters, dev)
+        sb.cg_solve(f, op, topo, sb.CgConfig(3, 0.0), workspace=ws)
+        torch.cuda.synchronize(dev)
+        ev0.record()
+        res = sb.cg_solve(f, op, topo, sb.CgConfig(iters, 0.0), workspace=ws)
+        ev1.record()
+        torch.cuda.synchronize(dev)
+        hist_last = float(res.residual_history[-1])
+        path = "fused single-GPU solver (sem_cg_run)"
+    else:
+        part = SlabPartition(ex, ey, ez, n, world, rank)
+        e0, e1 = part.element_range
+        # this rank's slice of the global inputs, generated in place
+        mesh_l = sb.build_mesh(ex, ey, part.ez, n, 1.0)
+        geom_l = sb.build_geom(mesh_l, b, device=dev)  # affine box: identical per element
+        f_g = None
+        topo_g = sb.build_topology(sb.build_mesh(ex, ey, ez, n, 1.0))
+        f_g = sb.make_rhs(e_total, n, topo_g, sb.mix64(1, e_total), device=dev) \
+            if e_total * n ** 3 * 8 * 2 < 40e9 else None
+        f_l = f_g[e0:e1].contiguous()
+        del f_g
+        comm = SlabComm(part)
+        ops = CudaSlabOps(part, geom_l.values, b, iters, dev)
+        dist_cg_solve(ops, comm, f_l, 3)
+        torch.cuda.synchronize(dev)
+        dist.barrier(device_ids=[dev.index])
+        ev0.record()
+        res = dist_cg_solve(ops, comm, f_l, iters)
+        ev1.record()
+        torch.cuda.synchronize(dev)
+        hist_last = float(res.residual_history[-1])
+        path = "z-slab partition, NCCL halo (2 ordered P2P steps) + rank-ordered all_gather"
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    per_it = ms / iters
+    dofs_total = e_total * n ** 3
+    model = perf.model_flops_per_iteration(dofs_total, n) / (per_it * 1e-3)
+    return {"global_box": [ex, ey, ez], "elements_per_gpu": per, "iterations": iters,
+            "ms_per_iteration": per_it, "model_gflops_total": model / 1e9,
+            "model_gflops_per_gpu": model / 1e9 / world, "final_residual": hist_last,
+            "path": path, "timing": "CUDA events, max over ranks"}
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -370,6 +439,8 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cg", type=int, default=1)
+    ap.add_argument("--cg-weak", type=int, default=1)
+    ap.add_argument("--cg-weak-iters", type=int, default=100)
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -27,12 +27,15 @@ dssum_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t
                  const double* __restrict__ bot, const double* __restrict__ top)
 {
     constexpr int NN = N * N, NNN = N * N * N;
-    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    // work item = (element, chunk of <= kBoxThreads points): equal-size items balance
+    // the fixed grid (E*SPLIT items instead of E elements)
+    constexpr int SPLIT_ = (NNN + kBoxThreads - 1) / kBoxThreads, CHUNK_ = (NNN + SPLIT_ - 1) / SPLIT_;
+    for (int64_t it_ = blockIdx.x; it_ < E * SPLIT_; it_ += gridDim.x) {
+        const int64_t e = it_ / SPLIT_;
         const ElemCoord c = elem_coord(e, b);
-        #pragma unroll
-        for (int t_ = 0; t_ < (NNN + kBoxThreads - 1) / kBoxThreads; ++t_) {
-            const int r = threadIdx.x + t_ * kBoxThreads;
-            if (r >= NNN) break;
+        {
+            const int r = (int)(it_ - e * SPLIT_) * CHUNK_ + (int)threadIdx.x;
+            if ((int)threadIdx.x >= CHUNK_ || r >= NNN) continue;
             const int k = r / NN, j = (r / N) % N, i = r % N;
             double s;
             if (!slab_face_value<N>(c, i, j, k, b, bot, top, s)) s = gather_sum<N>(f, c, i, j, k, b);
@@ -47,12 +50,15 @@ __global__ void __launch_bounds__(kBoxThreads)
 mask_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, Box b)
 {
     constexpr int NN = N * N, NNN = N * N * N;
-    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    // work item = (element, chunk of <= kBoxThreads points): equal-size items balance
+    // the fixed grid (E*SPLIT items instead of E elements)
+    constexpr int SPLIT_ = (NNN + kBoxThreads - 1) / kBoxThreads, CHUNK_ = (NNN + SPLIT_ - 1) / SPLIT_;
+    for (int64_t it_ = blockIdx.x; it_ < E * SPLIT_; it_ += gridDim.x) {
+        const int64_t e = it_ / SPLIT_;
         const ElemCoord c = elem_coord(e, b);
-        #pragma unroll
-        for (int t_ = 0; t_ < (NNN + kBoxThreads - 1) / kBoxThreads; ++t_) {
-            const int r = threadIdx.x + t_ * kBoxThreads;
-            if (r >= NNN) break;
+        {
+            const int r = (int)(it_ - e * SPLIT_) * CHUNK_ + (int)threadIdx.x;
+            if ((int)threadIdx.x >= CHUNK_ || r >= NNN) continue;
             const int k = r / NN, j = (r / N) % N, i = r % N;
             out[e * NNN + r] = mul_rn(__ldg(f + e * NNN + r), mask_val<N>(c, i, j, k, b));
         }

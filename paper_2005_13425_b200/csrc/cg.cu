@@ -75,12 +75,15 @@ glsc3_box_kernel(const double* __restrict__ a, const double* __restrict__ b, int
 {
     constexpr int NN = N * N, NNN = N * N * N;
     double acc = 0.0;
-    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    // work item = (element, chunk of <= kReduceThreads points): equal-size items balance
+    // the fixed grid (E*SPLIT items instead of E elements)
+    constexpr int SPLIT_ = (NNN + kReduceThreads - 1) / kReduceThreads, CHUNK_ = (NNN + SPLIT_ - 1) / SPLIT_;
+    for (int64_t it_ = blockIdx.x; it_ < E * SPLIT_; it_ += gridDim.x) {
+        const int64_t e = it_ / SPLIT_;
         const ElemCoord c = elem_coord(e, bx);
-        #pragma unroll
-        for (int t_ = 0; t_ < (NNN + kReduceThreads - 1) / kReduceThreads; ++t_) {
-            const int q = threadIdx.x + t_ * kReduceThreads;
-            if (q >= NNN) break;
+        {
+            const int q = (int)(it_ - e * SPLIT_) * CHUNK_ + (int)threadIdx.x;
+            if ((int)threadIdx.x >= CHUNK_ || q >= NNN) continue;
             const int k = q / NN, j = (q / N) % N, i = q % N;
             const int64_t idx = e * NNN + q;
             acc += mul_rn(mul_rn(__ldg(a + idx), __ldg(b + idx)), inv_mult<N>(c, i, j, k, bx));
@@ -149,12 +152,15 @@ cg_init_kernel(const double* __restrict__ f, double* __restrict__ x, double* __r
 {
     constexpr int NN = N * N, NNN = N * N * N;
     double acc = 0.0;
-    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    // work item = (element, chunk of <= kReduceThreads points): equal-size items balance
+    // the fixed grid (E*SPLIT items instead of E elements)
+    constexpr int SPLIT_ = (NNN + kReduceThreads - 1) / kReduceThreads, CHUNK_ = (NNN + SPLIT_ - 1) / SPLIT_;
+    for (int64_t it_ = blockIdx.x; it_ < E * SPLIT_; it_ += gridDim.x) {
+        const int64_t e = it_ / SPLIT_;
         const ElemCoord c = elem_coord(e, bx);
-        #pragma unroll
-        for (int t_ = 0; t_ < (NNN + kReduceThreads - 1) / kReduceThreads; ++t_) {
-            const int q = threadIdx.x + t_ * kReduceThreads;
-            if (q >= NNN) break;
+        {
+            const int q = (int)(it_ - e * SPLIT_) * CHUNK_ + (int)threadIdx.x;
+            if ((int)threadIdx.x >= CHUNK_ || q >= NNN) continue;
             const int k = q / NN, j = (q / N) % N, i = q % N;
             const int64_t idx = e * NNN + q;
             const double rv = mul_rn(__ldg(f + idx), mask_val<N>(c, i, j, k, bx));
@@ -211,12 +217,15 @@ cg_assemble_kernel(const double* __restrict__ w, double* __restrict__ w2,
     constexpr int NN = N * N, NNN = N * N * N;
     if (st->stop) return;
     double acc = 0.0;
-    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    // work item = (element, chunk of <= kReduceThreads points): equal-size items balance
+    // the fixed grid (E*SPLIT items instead of E elements)
+    constexpr int SPLIT_ = (NNN + kReduceThreads - 1) / kReduceThreads, CHUNK_ = (NNN + SPLIT_ - 1) / SPLIT_;
+    for (int64_t it_ = blockIdx.x; it_ < E * SPLIT_; it_ += gridDim.x) {
+        const int64_t e = it_ / SPLIT_;
         const ElemCoord c = elem_coord(e, bx);
-        #pragma unroll
-        for (int t_ = 0; t_ < (NNN + kReduceThreads - 1) / kReduceThreads; ++t_) {
-            const int q = threadIdx.x + t_ * kReduceThreads;
-            if (q >= NNN) break;
+        {
+            const int q = (int)(it_ - e * SPLIT_) * CHUNK_ + (int)threadIdx.x;
+            if ((int)threadIdx.x >= CHUNK_ || q >= NNN) continue;
             const int k = q / NN, j = (q / N) % N, i = q % N;
             const int64_t idx = e * NNN + q;
             double sv;
@@ -245,12 +254,15 @@ cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* _
     if (st->stop) return;
     const double alpha = st->alpha, nalpha = -alpha;
     double acc = 0.0;
-    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    // work item = (element, chunk of <= kReduceThreads points): equal-size items balance
+    // the fixed grid (E*SPLIT items instead of E elements)
+    constexpr int SPLIT_ = (NNN + kReduceThreads - 1) / kReduceThreads, CHUNK_ = (NNN + SPLIT_ - 1) / SPLIT_;
+    for (int64_t it_ = blockIdx.x; it_ < E * SPLIT_; it_ += gridDim.x) {
+        const int64_t e = it_ / SPLIT_;
         const ElemCoord c = elem_coord(e, bx);
-        #pragma unroll
-        for (int t_ = 0; t_ < (NNN + kReduceThreads - 1) / kReduceThreads; ++t_) {
-            const int q = threadIdx.x + t_ * kReduceThreads;
-            if (q >= NNN) break;
+        {
+            const int q = (int)(it_ - e * SPLIT_) * CHUNK_ + (int)threadIdx.x;
+            if ((int)threadIdx.x >= CHUNK_ || q >= NNN) continue;
             const int k = q / NN, j = (q / N) % N, i = q % N;
             const int64_t idx = e * NNN + q;
             x[idx] = add_rn(x[idx], mul_rn(alpha, __ldg(p + idx)));
