@@ -15,60 +15,57 @@
 // from coordinates, so no index array is read.
 #include "box.cuh"
 #include "reduce.cuh"
+#include "rows.cuh"
 
 namespace sem {
 
-constexpr int kBoxThreads = 256;
 
 // MASK: multiply by the 0/1 mask (reference mask() is f*mask).
 template <int N, bool MASK>
-__global__ void __launch_bounds__(kBoxThreads)
+__global__ void __launch_bounds__(kRowThreads)
 dssum_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, Box b,
                  const double* __restrict__ bot, const double* __restrict__ top)
 {
     constexpr int NN = N * N, NNN = N * N * N;
-    // work item = (element, chunk of <= kBoxThreads points): equal-size items balance
-    // the fixed grid (E*SPLIT items instead of E elements)
-    constexpr int SPLIT_ = (NNN + kBoxThreads - 1) / kBoxThreads, CHUNK_ = (NNN + SPLIT_ - 1) / SPLIT_;
-    for (int64_t it_ = blockIdx.x; it_ < E * SPLIT_; it_ += gridDim.x) {
-        const int64_t e = it_ / SPLIT_;
-        const ElemCoord c = elem_coord(e, b);
-        {
-            const int r = (int)(it_ - e * SPLIT_) * CHUNK_ + (int)threadIdx.x;
-            if ((int)threadIdx.x >= CHUNK_ || r >= NNN) continue;
-            const int k = r / NN, j = (r / N) % N, i = r % N;
-            double s;
-            if (!slab_face_value<N>(c, i, j, k, b, bot, top, s)) s = gather_sum<N>(f, c, i, j, k, b);
-            if (MASK) s = mul_rn(s, mask_val<N>(c, i, j, k, b));
-            out[e * NNN + r] = s;
+    const int64_t rows = E * NN;
+    for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < rows;
+         row += (int64_t)gridDim.x * kRowThreads) {
+        const Row<N> r = make_row<N>(row, b);
+        double v[N];
+        dssum_row<N>(f, r, b, bot, top, v);
+        if (MASK) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) v[i] = mul_rn(v[i], row_mask<N>(r, i));
         }
+        store_row<N>(out + r.e * NNN + r.jk * N, v);
     }
 }
 
 template <int N>
-__global__ void __launch_bounds__(kBoxThreads)
+__global__ void __launch_bounds__(kRowThreads)
 mask_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, Box b)
 {
     constexpr int NN = N * N, NNN = N * N * N;
-    // work item = (element, chunk of <= kBoxThreads points): equal-size items balance
-    // the fixed grid (E*SPLIT items instead of E elements)
-    constexpr int SPLIT_ = (NNN + kBoxThreads - 1) / kBoxThreads, CHUNK_ = (NNN + SPLIT_ - 1) / SPLIT_;
-    for (int64_t it_ = blockIdx.x; it_ < E * SPLIT_; it_ += gridDim.x) {
-        const int64_t e = it_ / SPLIT_;
-        const ElemCoord c = elem_coord(e, b);
-        {
-            const int r = (int)(it_ - e * SPLIT_) * CHUNK_ + (int)threadIdx.x;
-            if ((int)threadIdx.x >= CHUNK_ || r >= NNN) continue;
-            const int k = r / NN, j = (r / N) % N, i = r % N;
-            out[e * NNN + r] = mul_rn(__ldg(f + e * NNN + r), mask_val<N>(c, i, j, k, b));
-        }
+    const int64_t rows = E * NN;
+    for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < rows;
+         row += (int64_t)gridDim.x * kRowThreads) {
+        const Row<N> r = make_row<N>(row, b);
+        double v[N];
+        load_row<N>(f + r.e * NNN + r.jk * N, v);
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = mul_rn(v[i], row_mask<N>(r, i));
+        store_row<N>(out + r.e * NNN + r.jk * N, v);
     }
 }
 
+template <int N>
 static unsigned box_grid(int64_t E)
 {
+    const int64_t rows = E * N * N;
+    int64_t blocks = (rows + kRowThreads - 1) / kRowThreads;
     const int64_t cap = 16LL * sm_count();
-    return (unsigned)(E < cap ? (E > 0 ? E : 1) : cap);
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks > 0 ? blocks : 1);
 }
 
 template <int N>
@@ -77,9 +74,9 @@ static int launch_dssum(const double* f, double* out, int64_t E, Box b, bool mas
 {
     if (E == 0) return 0;
     if (mask)
-        dssum_box_kernel<N, true><<<box_grid(E), kBoxThreads, 0, s>>>(f, out, E, b, bot, top);
+        dssum_box_kernel<N, true><<<box_grid<N>(E), kRowThreads, 0, s>>>(f, out, E, b, bot, top);
     else
-        dssum_box_kernel<N, false><<<box_grid(E), kBoxThreads, 0, s>>>(f, out, E, b, bot, top);
+        dssum_box_kernel<N, false><<<box_grid<N>(E), kRowThreads, 0, s>>>(f, out, E, b, bot, top);
     SEM_CHECK_LAUNCH("sem_dssum_box launch");
     return 0;
 }
@@ -88,7 +85,7 @@ template <int N>
 static int launch_mask(const double* f, double* out, int64_t E, Box b, cudaStream_t s)
 {
     if (E == 0) return 0;
-    mask_box_kernel<N><<<box_grid(E), kBoxThreads, 0, s>>>(f, out, E, b);
+    mask_box_kernel<N><<<box_grid<N>(E), kRowThreads, 0, s>>>(f, out, E, b);
     SEM_CHECK_LAUNCH("sem_mask_box launch");
     return 0;
 }

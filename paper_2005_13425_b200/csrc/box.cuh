@@ -67,76 +67,6 @@ __device__ __forceinline__ ElemCoord elem_coord(int64_t e, const Box& b)
     return c;
 }
 
-// 1/multiplicity of local point (i,j,k) of element c: exact power of two.
-template <int N>
-__device__ __forceinline__ double inv_mult(const ElemCoord& c, int i, int j, int k, const Box& b)
-{
-    const int m = axis_mult<N>(c.ix, i, b.ex) * axis_mult<N>(c.iy, j, b.ey) *
-                  axis_mult<N>(c.iz + b.gz0, k, b.ez_global);
-    return m == 1 ? 1.0 : (m == 2 ? 0.5 : (m == 4 ? 0.25 : 0.125));
-}
-
-template <int N>
-__device__ __forceinline__ double mask_val(const ElemCoord& c, int i, int j, int k, const Box& b)
-{
-    return (axis_interior<N>(c.ix, i, b.ex) && axis_interior<N>(c.iy, j, b.ey) &&
-            axis_interior<N>(c.iz + b.gz0, k, b.ez_global))
-               ? 1.0
-               : 0.0;
-}
-
-// Ordered gather of every copy of local point (i,j,k) of element c (the
-// bincount order of assembly.py:116: ascending element id, from +0.0).
-template <int N>
-__device__ __forceinline__ double gather_sum(const double* __restrict__ f, const ElemCoord& c,
-                                             int i, int j, int k, const Box& b)
-{
-    constexpr int NNN = N * N * N;
-    const AxisCopies ax = axis_copies<N>(c.ix, i, b.ex);
-    const AxisCopies ay = axis_copies<N>(c.iy, j, b.ey);
-    const AxisCopies az = axis_copies<N>(c.iz, k, b.ez);
-    // issue every copy's load first (predicated), then add in the
-    // reference order: z-choice outer, y middle, x inner = ascending e
-    double v[8];
-    bool ok[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int zc = q >> 2, yc = (q >> 1) & 1, xc = q & 1;
-        ok[q] = zc < az.cnt && yc < ay.cnt && xc < ax.cnt;
-        const int ez_ = zc ? az.e1 : az.e0, kk = zc ? az.l1 : az.l0;
-        const int ey_ = yc ? ay.e1 : ay.e0, jj = yc ? ay.l1 : ay.l0;
-        const int ex_ = xc ? ax.e1 : ax.e0, ii = xc ? ax.l1 : ax.l0;
-        const int64_t e2 = ((int64_t)ez_ * b.ey + ey_) * b.ex + ex_;
-        v[q] = ok[q] ? __ldg(f + e2 * NNN + (kk * N + jj) * N + ii) : 0.0;
-    }
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-        if (ok[q]) s = add_rn(s, v[q]);
-    return s;
-}
-
-// Multi-GPU z-slabs: the field holds global element layers [gz0, gz0+ez).
-// Nodes on a slab face shared with a neighbouring rank take their assembled
-// value from a plane of totals exchanged by the halo protocol (dist.py);
-// plane index = gy * (ex*(n-1)+1) + gx over the global x/y lattice.
-template <int N>
-__device__ __forceinline__ bool slab_face_value(const ElemCoord& c, int i, int j, int k,
-                                                const Box& b, const double* __restrict__ bot,
-                                                const double* __restrict__ top, double& v)
-{
-    const int nx = b.ex * (N - 1) + 1;
-    if (bot != nullptr && c.iz == 0 && k == 0) {
-        v = __ldg(bot + (int64_t)(c.iy * (N - 1) + j) * nx + (c.ix * (N - 1) + i));
-        return true;
-    }
-    if (top != nullptr && c.iz == b.ez - 1 && k == N - 1) {
-        v = __ldg(top + (int64_t)(c.iy * (N - 1) + j) * nx + (c.ix * (N - 1) + i));
-        return true;
-    }
-    return false;
-}
-
 // Dispatch a runtime n in [2,16] to a compile-time NV.
 #define SEM_SWITCH_N(n, ...)                                                          \
     switch (n) {                                                                      \
