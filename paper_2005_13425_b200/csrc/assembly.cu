@@ -15,57 +15,46 @@
 // from coordinates, so no index array is read.
 #include "box.cuh"
 #include "reduce.cuh"
-#include "rows.cuh"
+#include "cols.cuh"
 
 namespace sem {
 
 
 // MASK: multiply by the 0/1 mask (reference mask() is f*mask).
 template <int N, bool MASK>
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(ColCfg<N>::THREADS)
 dssum_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, Box b,
                  const double* __restrict__ bot, const double* __restrict__ top)
 {
     constexpr int NN = N * N, NNN = N * N * N;
-    const int64_t rows = E * NN;
-    for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < rows;
-         row += (int64_t)gridDim.x * kRowThreads) {
-        const Row<N> r = make_row<N>(row, b);
-        double v[N];
-        dssum_row<N>(f, r, b, bot, top, v);
-        if (MASK) {
+    col_loop<N>(E, b, [&](int64_t e, const ElemCoord& c, const ColXY<N>& t) {
 #pragma unroll
-            for (int i = 0; i < N; ++i) v[i] = mul_rn(v[i], row_mask<N>(r, i));
+        for (int k = 0; k < N; ++k) {
+            double s = col_dssum<N>(f, t, c, k, b, bot, top);
+            if (MASK) s = mul_rn(s, col_mask<N>(t, c, k, b));
+            out[e * NNN + k * NN + t.p] = s;
         }
-        store_row<N>(out + r.e * NNN + r.jk * N, v);
-    }
+    });
 }
 
 template <int N>
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(ColCfg<N>::THREADS)
 mask_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, Box b)
 {
     constexpr int NN = N * N, NNN = N * N * N;
-    const int64_t rows = E * NN;
-    for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < rows;
-         row += (int64_t)gridDim.x * kRowThreads) {
-        const Row<N> r = make_row<N>(row, b);
-        double v[N];
-        load_row<N>(f + r.e * NNN + r.jk * N, v);
+    col_loop<N>(E, b, [&](int64_t e, const ElemCoord& c, const ColXY<N>& t) {
 #pragma unroll
-        for (int i = 0; i < N; ++i) v[i] = mul_rn(v[i], row_mask<N>(r, i));
-        store_row<N>(out + r.e * NNN + r.jk * N, v);
-    }
+        for (int k = 0; k < N; ++k) {
+            const int64_t idx = e * NNN + k * NN + t.p;
+            out[idx] = mul_rn(__ldg(f + idx), col_mask<N>(t, c, k, b));
+        }
+    });
 }
 
 template <int N>
 static unsigned box_grid(int64_t E)
 {
-    const int64_t rows = E * N * N;
-    int64_t blocks = (rows + kRowThreads - 1) / kRowThreads;
-    const int64_t cap = 16LL * sm_count();
-    if (blocks > cap) blocks = cap;
-    return (unsigned)(blocks > 0 ? blocks : 1);
+    return col_grid<N>(E, 16 * sm_count());
 }
 
 template <int N>
@@ -74,9 +63,9 @@ static int launch_dssum(const double* f, double* out, int64_t E, Box b, bool mas
 {
     if (E == 0) return 0;
     if (mask)
-        dssum_box_kernel<N, true><<<box_grid<N>(E), kRowThreads, 0, s>>>(f, out, E, b, bot, top);
+        dssum_box_kernel<N, true><<<box_grid<N>(E), ColCfg<N>::THREADS, 0, s>>>(f, out, E, b, bot, top);
     else
-        dssum_box_kernel<N, false><<<box_grid<N>(E), kRowThreads, 0, s>>>(f, out, E, b, bot, top);
+        dssum_box_kernel<N, false><<<box_grid<N>(E), ColCfg<N>::THREADS, 0, s>>>(f, out, E, b, bot, top);
     SEM_CHECK_LAUNCH("sem_dssum_box launch");
     return 0;
 }
@@ -85,7 +74,7 @@ template <int N>
 static int launch_mask(const double* f, double* out, int64_t E, Box b, cudaStream_t s)
 {
     if (E == 0) return 0;
-    mask_box_kernel<N><<<box_grid<N>(E), kRowThreads, 0, s>>>(f, out, E, b);
+    mask_box_kernel<N><<<box_grid<N>(E), ColCfg<N>::THREADS, 0, s>>>(f, out, E, b);
     SEM_CHECK_LAUNCH("sem_mask_box launch");
     return 0;
 }
