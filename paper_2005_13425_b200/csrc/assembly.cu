@@ -15,46 +15,58 @@
 // from coordinates, so no index array is read.
 #include "box.cuh"
 #include "reduce.cuh"
-#include "cols.cuh"
+#include "flat.cuh"
+#include "rows.cuh"
 
 namespace sem {
 
 
 // MASK: multiply by the 0/1 mask (reference mask() is f*mask).
 template <int N, bool MASK>
-__global__ void __launch_bounds__(ColCfg<N>::THREADS)
+__global__ void __launch_bounds__(kRowThreads)
 dssum_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, Box b,
                  const double* __restrict__ bot, const double* __restrict__ top)
 {
     constexpr int NN = N * N, NNN = N * N * N;
-    col_loop<N>(E, b, [&](int64_t e, const ElemCoord& c, const ColXY<N>& t) {
+    for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < E * NN;
+         row += (int64_t)gridDim.x * kRowThreads) {
+        const Row<N> r = make_row<N>(row, b);
+        double v[N];
+        dssum_row<N>(f, r, b, bot, top, v);
+        if (MASK) {
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            double s = col_dssum<N>(f, t, c, k, b, bot, top);
-            if (MASK) s = mul_rn(s, col_mask<N>(t, c, k, b));
-            out[e * NNN + k * NN + t.p] = s;
+            for (int i = 0; i < N; ++i) v[i] = mul_rn(v[i], row_mask<N>(r, i));
         }
-    });
+        store_row<N>(out + r.e * NNN + r.jk * N, v);
+    }
 }
 
 template <int N>
-__global__ void __launch_bounds__(ColCfg<N>::THREADS)
-mask_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, Box b)
+__global__ void __launch_bounds__(PairCfg<N>::THREADS)
+mask_box_kernel(const double* __restrict__ f, double* __restrict__ out, int64_t E, BoxFlat bf)
 {
-    constexpr int NN = N * N, NNN = N * N * N;
-    col_loop<N>(E, b, [&](int64_t e, const ElemCoord& c, const ColXY<N>& t) {
+    constexpr int NP = PairCfg<N>::NP;
+    const int64_t units = E * (int64_t)(N * N * N) / NP;
+    for (int64_t u = (int64_t)blockIdx.x * PairCfg<N>::THREADS + threadIdx.x; u < units;
+         u += (int64_t)gridDim.x * PairCfg<N>::THREADS) {
+        const int64_t q0 = u * NP;
+        ElemCoord c;
+        int i, j, k;
+        pair_point<N>(q0, bf, c, i, j, k);
+        double v[NP];
+        ld_pair<N>(f + q0, v);
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const int64_t idx = e * NNN + k * NN + t.p;
-            out[idx] = mul_rn(__ldg(f + idx), col_mask<N>(t, c, k, b));
-        }
-    });
+        for (int h = 0; h < NP; ++h) v[h] = mul_rn(v[h], mask_of<N>(c, i + h, j, k, bf.b));
+        st_pair<N>(out + q0, v);
+    }
 }
 
 template <int N>
 static unsigned box_grid(int64_t E)
 {
-    return col_grid<N>(E, 16 * sm_count());
+    const int64_t blocks = (E * N * N + kRowThreads - 1) / kRowThreads;
+    const int64_t cap = 16LL * sm_count();
+    return (unsigned)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
 }
 
 template <int N>
@@ -63,9 +75,9 @@ static int launch_dssum(const double* f, double* out, int64_t E, Box b, bool mas
 {
     if (E == 0) return 0;
     if (mask)
-        dssum_box_kernel<N, true><<<box_grid<N>(E), ColCfg<N>::THREADS, 0, s>>>(f, out, E, b, bot, top);
+        dssum_box_kernel<N, true><<<box_grid<N>(E), kRowThreads, 0, s>>>(f, out, E, b, bot, top);
     else
-        dssum_box_kernel<N, false><<<box_grid<N>(E), ColCfg<N>::THREADS, 0, s>>>(f, out, E, b, bot, top);
+        dssum_box_kernel<N, false><<<box_grid<N>(E), kRowThreads, 0, s>>>(f, out, E, b, bot, top);
     SEM_CHECK_LAUNCH("sem_dssum_box launch");
     return 0;
 }
@@ -74,7 +86,8 @@ template <int N>
 static int launch_mask(const double* f, double* out, int64_t E, Box b, cudaStream_t s)
 {
     if (E == 0) return 0;
-    mask_box_kernel<N><<<box_grid<N>(E), ColCfg<N>::THREADS, 0, s>>>(f, out, E, b);
+    mask_box_kernel<N><<<flat_grid<N>(E, 16 * sm_count()), PairCfg<N>::THREADS, 0, s>>>(
+        f, out, E, make_box_flat(b));
     SEM_CHECK_LAUNCH("sem_mask_box launch");
     return 0;
 }

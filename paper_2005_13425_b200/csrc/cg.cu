@@ -17,7 +17,8 @@
 
 #include "box.cuh"
 #include "reduce.cuh"
-#include "cols.cuh"
+#include "flat.cuh"
+#include "rows.cuh"
 
 namespace sem {
 
@@ -65,27 +66,37 @@ glsc3_kernel(const double* __restrict__ a, const double* __restrict__ b,
     reduce_publish_and_finish<1, kReduceThreads>(vals, rs, [&](const double (&t)[1]) { *out = t[0]; });
 }
 
-// Box-weighted dot, column-mapped (cols.cuh): w = 1/multiplicity from the
-// lattice.  The loop nest (and so the summation order) is shared with the
+// Box-weighted dot over flat point pairs (flat.cuh): w = 1/multiplicity from
+// the lattice.  The loop nest (and so the summation order) is shared with the
 // fused CG kernels below, so weighted_dot reproduces their reductions
 // bit-for-bit.
+#define SEM_PAIR_LOOP(E_)                                                              \
+    constexpr int NP = PairCfg<N>::NP;                                                 \
+    const int64_t units_ = (E_) * (int64_t)(N * N * N) / NP;                           \
+    for (int64_t u_ = (int64_t)blockIdx.x * PairCfg<N>::THREADS + threadIdx.x; u_ < units_; \
+         u_ += (int64_t)gridDim.x * PairCfg<N>::THREADS)
+
 template <int N>
-__global__ void __launch_bounds__(ColCfg<N>::THREADS)
-glsc3_box_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t E, Box bx,
-                 double* out, ReduceScratch* rs)
+__global__ void __launch_bounds__(PairCfg<N>::THREADS)
+glsc3_box_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t E,
+                 BoxFlat bf, double* out, ReduceScratch* rs)
 {
-    constexpr int NN = N * N, NNN = N * N * N;
     double acc = 0.0;
-    col_loop<N>(E, bx, [&](int64_t e, const ElemCoord& c, const ColXY<N>& t) {
+    SEM_PAIR_LOOP(E) {
+        const int64_t q0 = u_ * NP;
+        ElemCoord c;
+        int i, j, k;
+        pair_point<N>(q0, bf, c, i, j, k);
+        double va[NP], vb[NP];
+        ld_pair<N>(a + q0, va);
+        ld_pair<N>(b + q0, vb);
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const int64_t idx = e * NNN + k * NN + t.p;
-            acc += mul_rn(mul_rn(__ldg(a + idx), __ldg(b + idx)), col_inv_mult<N>(t, c, k, bx));
-        }
-    });
+        for (int h = 0; h < NP; ++h)
+            acc += mul_rn(mul_rn(va[h], vb[h]), inv_mult_of<N>(c, i + h, j, k, bf.b));
+    }
     const double vals[1] = {acc};
-    reduce_publish_and_finish<1, ColCfg<N>::THREADS>(vals, rs,
-                                                     [&](const double (&tt)[1]) { *out = tt[0]; });
+    reduce_publish_and_finish<1, PairCfg<N>::THREADS>(vals, rs,
+                                                      [&](const double (&tt)[1]) { *out = tt[0]; });
 }
 
 // ------------------------------------------------------------ CG kernels --
@@ -140,26 +151,31 @@ __device__ __forceinline__ void fin_phase(sem_cg_state* st, int phase, double to
 
 // init: r = mask(f) (assembly.py:123-129), x = p = 0, rtz = <r,r>_c.
 template <int N, bool DIST>
-__global__ void __launch_bounds__(ColCfg<N>::THREADS)
+__global__ void __launch_bounds__(PairCfg<N>::THREADS)
 cg_init_kernel(const double* __restrict__ f, double* __restrict__ x, double* __restrict__ r,
-               double* __restrict__ p, int64_t E, Box bx, sem_cg_state* st, ReduceScratch* rs,
-               int max_iterations, double tolerance)
+               double* __restrict__ p, int64_t E, BoxFlat bf, sem_cg_state* st,
+               ReduceScratch* rs, int max_iterations, double tolerance)
 {
-    constexpr int NN = N * N, NNN = N * N * N;
     double acc = 0.0;
-    col_loop<N>(E, bx, [&](int64_t e, const ElemCoord& c, const ColXY<N>& t) {
+    SEM_PAIR_LOOP(E) {
+        const int64_t q0 = u_ * NP;
+        ElemCoord c;
+        int i, j, k;
+        pair_point<N>(q0, bf, c, i, j, k);
+        double fv[NP], z[NP];
+        ld_pair<N>(f + q0, fv);
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const int64_t idx = e * NNN + k * NN + t.p;
-            const double rv = mul_rn(__ldg(f + idx), col_mask<N>(t, c, k, bx));
-            r[idx] = rv;
-            x[idx] = 0.0;
-            p[idx] = 0.0;
-            acc += mul_rn(mul_rn(rv, rv), col_inv_mult<N>(t, c, k, bx));
+        for (int h = 0; h < NP; ++h) {
+            fv[h] = mul_rn(fv[h], mask_of<N>(c, i + h, j, k, bf.b));
+            z[h] = 0.0;
+            acc += mul_rn(mul_rn(fv[h], fv[h]), inv_mult_of<N>(c, i + h, j, k, bf.b));
         }
-    });
+        st_pair<N>(r + q0, fv);
+        st_pair<N>(x + q0, z);
+        st_pair<N>(p + q0, z);
+    }
     const double vals[1] = {acc};
-    reduce_publish_and_finish<1, ColCfg<N>::THREADS>(vals, rs, [&](const double (&t)[1]) {
+    reduce_publish_and_finish<1, PairCfg<N>::THREADS>(vals, rs, [&](const double (&t)[1]) {
         st->max_iterations = max_iterations;
         st->tolerance = tolerance;
         if (DIST) {
@@ -196,7 +212,7 @@ cg_p_kernel(double* __restrict__ p, const double* __restrict__ r, int64_t m, sem
 
 // w2 = mask(dssum(w)) and <p, w2>_c (assembly.py:113-129 + cg.py:163-170).
 template <int N, bool DIST>
-__global__ void __launch_bounds__(ColCfg<N>::THREADS)
+__global__ void __launch_bounds__(kRowThreads)
 cg_assemble_kernel(const double* __restrict__ w, double* __restrict__ w2,
                    const double* __restrict__ p, int64_t E, Box bx, sem_cg_state* st,
                    ReduceScratch* rs, const double* __restrict__ bot,
@@ -205,19 +221,22 @@ cg_assemble_kernel(const double* __restrict__ w, double* __restrict__ w2,
     constexpr int NN = N * N, NNN = N * N * N;
     if (st->stop) return;
     double acc = 0.0;
-    col_loop<N>(E, bx, [&](int64_t e, const ElemCoord& c, const ColXY<N>& t) {
+    for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < E * NN;
+         row += (int64_t)gridDim.x * kRowThreads) {
+        const Row<N> rw = make_row<N>(row, bx);
+        const int64_t base = rw.e * NNN + rw.jk * N;
+        double v[N], pv[N];
+        dssum_row<N>(w, rw, bx, DIST ? bot : nullptr, DIST ? top : nullptr, v);
+        load_row<N>(p + base, pv);
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const int64_t idx = e * NNN + k * NN + t.p;
-            const double v = mul_rn(col_dssum<N>(w, t, c, k, bx, DIST ? bot : nullptr,
-                                                 DIST ? top : nullptr),
-                                    col_mask<N>(t, c, k, bx));
-            w2[idx] = v;
-            acc += mul_rn(mul_rn(__ldg(p + idx), v), col_inv_mult<N>(t, c, k, bx));
+        for (int i = 0; i < N; ++i) {
+            v[i] = mul_rn(v[i], row_mask<N>(rw, i));
+            acc += mul_rn(mul_rn(pv[i], v[i]), row_inv_mult<N>(rw, i));
         }
-    });
+        store_row<N>(w2 + base, v);
+    }
     const double vals[1] = {acc};
-    reduce_publish_and_finish<1, ColCfg<N>::THREADS>(vals, rs, [&](const double (&t)[1]) {
+    reduce_publish_and_finish<1, kRowThreads>(vals, rs, [&](const double (&t)[1]) {
         if (DIST) st->local_sum = t[0];
         else fin_pap(st, t[0]);
     });
@@ -225,27 +244,35 @@ cg_assemble_kernel(const double* __restrict__ w, double* __restrict__ w2,
 
 // x += alpha p ; r += (-alpha) w2 ; rnorm = sqrt(<r,r>_c)  (cg.py:170-186).
 template <int N, bool DIST>
-__global__ void __launch_bounds__(ColCfg<N>::THREADS)
+__global__ void __launch_bounds__(PairCfg<N>::THREADS)
 cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                 const double* __restrict__ w2, int64_t E, Box bx, sem_cg_state* st,
+                 const double* __restrict__ w2, int64_t E, BoxFlat bf, sem_cg_state* st,
                  double* history, ReduceScratch* rs)
 {
-    constexpr int NN = N * N, NNN = N * N * N;
     if (st->stop) return;
     const double alpha = st->alpha, nalpha = -alpha;
     double acc = 0.0;
-    col_loop<N>(E, bx, [&](int64_t e, const ElemCoord& c, const ColXY<N>& t) {
+    SEM_PAIR_LOOP(E) {
+        const int64_t q0 = u_ * NP;
+        ElemCoord c;
+        int i, j, k;
+        pair_point<N>(q0, bf, c, i, j, k);
+        double xv[NP], rv[NP], pv[NP], wv[NP];
+        ld_pair_rw<N>(x + q0, xv);
+        ld_pair_rw<N>(r + q0, rv);
+        ld_pair<N>(p + q0, pv);
+        ld_pair<N>(w2 + q0, wv);
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const int64_t idx = e * NNN + k * NN + t.p;
-            x[idx] = add_rn(x[idx], mul_rn(alpha, __ldg(p + idx)));
-            const double rv = add_rn(r[idx], mul_rn(nalpha, __ldg(w2 + idx)));
-            r[idx] = rv;
-            acc += mul_rn(mul_rn(rv, rv), col_inv_mult<N>(t, c, k, bx));
+        for (int h = 0; h < NP; ++h) {
+            xv[h] = add_rn(xv[h], mul_rn(alpha, pv[h]));
+            rv[h] = add_rn(rv[h], mul_rn(nalpha, wv[h]));
+            acc += mul_rn(mul_rn(rv[h], rv[h]), inv_mult_of<N>(c, i + h, j, k, bf.b));
         }
-    });
+        st_pair<N>(x + q0, xv);
+        st_pair<N>(r + q0, rv);
+    }
     const double vals[1] = {acc};
-    reduce_publish_and_finish<1, ColCfg<N>::THREADS>(vals, rs, [&](const double (&t)[1]) {
+    reduce_publish_and_finish<1, PairCfg<N>::THREADS>(vals, rs, [&](const double (&t)[1]) {
         if (DIST) st->local_sum = t[0];
         else fin_rr(st, t[0], history);
     });
@@ -253,10 +280,19 @@ cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* _
 
 // fixed-size grid for the row reductions (a function of E and n only, so
 // the reduction tree -- and every result -- is reproducible)
+// fixed grids for the reductions (functions of E and n only, so the
+// reduction trees -- and every result -- are reproducible)
 template <int N>
 static unsigned red_grid(int64_t E)
 {
-    return col_grid<N>(E, kReduceBlocks);
+    return flat_grid<N>(E, kReduceBlocks);
+}
+
+template <int N>
+static unsigned row_grid(int64_t E)
+{
+    const int64_t blocks = (E * N * N + kRowThreads - 1) / kRowThreads;
+    return (unsigned)(blocks < kReduceBlocks ? (blocks > 0 ? blocks : 1) : kReduceBlocks);
 }
 
 template <int N>
@@ -264,7 +300,7 @@ static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_st
                      int64_t E, Box bx, ReduceScratch* rs, int max_it, double tol,
                      cudaStream_t s)
 {
-    cg_init_kernel<N, false><<<red_grid<N>(E), ColCfg<N>::THREADS, 0, s>>>(f, x, r, p, E, bx, st, rs,
+    cg_init_kernel<N, false><<<red_grid<N>(E), PairCfg<N>::THREADS, 0, s>>>(f, x, r, p, E, make_box_flat(bx), st, rs,
                                                                      max_it, tol);
     SEM_CHECK_LAUNCH("sem_cg_init launch");
     return 0;
@@ -281,10 +317,10 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
         cg_p_kernel<<<vec_grid(m), kVecThreads, 0, s>>>(p, r, m, st, history);
         SEM_CHECK_LAUNCH("cg_p_kernel");
         if (int rc = ax_dispatch(p, g, dx, w, E, N, 0, s)) return rc;
-        cg_assemble_kernel<N, false><<<red_grid<N>(E), ColCfg<N>::THREADS, 0, s>>>(w, w2, p, E, bx, st,
+        cg_assemble_kernel<N, false><<<row_grid<N>(E), kRowThreads, 0, s>>>(w, w2, p, E, bx, st,
                                                                              rs, nullptr, nullptr);
         SEM_CHECK_LAUNCH("cg_assemble_kernel");
-        cg_update_kernel<N, false><<<red_grid<N>(E), ColCfg<N>::THREADS, 0, s>>>(x, r, p, w2, E, bx,
+        cg_update_kernel<N, false><<<red_grid<N>(E), PairCfg<N>::THREADS, 0, s>>>(x, r, p, w2, E, make_box_flat(bx),
                                                                            st, history, rs);
         SEM_CHECK_LAUNCH("cg_update_kernel");
     }
@@ -348,7 +384,7 @@ extern "C" int sem_glsc3_box(const double* a, const double* b, int32_t ex, int32
     const int64_t E = (int64_t)ex * ey * ez;
     auto* rs = static_cast<ReduceScratch*>(scratch);
     SEM_SWITCH_N(n, {
-        glsc3_box_kernel<NV><<<red_grid<NV>(E), ColCfg<NV>::THREADS, 0, s>>>(a, b, E, bx, out_dev, rs);
+        glsc3_box_kernel<NV><<<red_grid<NV>(E), PairCfg<NV>::THREADS, 0, s>>>(a, b, E, make_box_flat(bx), out_dev, rs);
         SEM_CHECK_LAUNCH("sem_glsc3_box launch");
         return 0;
     });
@@ -449,8 +485,8 @@ extern "C" int sem_cg_init_slab(const double* f, double* x, double* r, double* p
     const int64_t E = (int64_t)ex * ey * ez;
     auto* rs = static_cast<ReduceScratch*>(scratch);
     SEM_SWITCH_N(n, {
-        cg_init_kernel<NV, true><<<red_grid<NV>(E), ColCfg<NV>::THREADS, 0, s>>>(
-            f, x, r, p, E, bx, state, rs, max_iterations, tolerance);
+        cg_init_kernel<NV, true><<<red_grid<NV>(E), PairCfg<NV>::THREADS, 0, s>>>(
+            f, x, r, p, E, make_box_flat(bx), state, rs, max_iterations, tolerance);
         SEM_CHECK_LAUNCH("sem_cg_init_slab launch");
         return 0;
     });
@@ -487,7 +523,7 @@ extern "C" int sem_cg_assemble_slab(const double* w, double* w2, const double* p
     const int64_t E = (int64_t)ex * ey * ez;
     auto* rs = static_cast<ReduceScratch*>(scratch);
     SEM_SWITCH_N(n, {
-        cg_assemble_kernel<NV, true><<<red_grid<NV>(E), ColCfg<NV>::THREADS, 0, s>>>(
+        cg_assemble_kernel<NV, true><<<row_grid<NV>(E), kRowThreads, 0, s>>>(
             w, w2, p, E, bx, state, rs, bottom_totals, top_totals);
         SEM_CHECK_LAUNCH("sem_cg_assemble_slab launch");
         return 0;
@@ -510,8 +546,8 @@ extern "C" int sem_cg_update_slab(double* x, double* r, const double* p, const d
     const int64_t E = (int64_t)ex * ey * ez;
     auto* rs = static_cast<ReduceScratch*>(scratch);
     SEM_SWITCH_N(n, {
-        cg_update_kernel<NV, true><<<red_grid<NV>(E), ColCfg<NV>::THREADS, 0, s>>>(
-            x, r, p, w2, E, bx, state, nullptr, rs);
+        cg_update_kernel<NV, true><<<red_grid<NV>(E), PairCfg<NV>::THREADS, 0, s>>>(
+            x, r, p, w2, E, make_box_flat(bx), state, nullptr, rs);
         SEM_CHECK_LAUNCH("sem_cg_update_slab launch");
         return 0;
     });
@@ -546,7 +582,7 @@ extern "C" int sem_glsc3_slab(const double* a, const double* b, int32_t ex, int3
     const int64_t E = (int64_t)ex * ey * ez;
     auto* rs = static_cast<ReduceScratch*>(scratch);
     SEM_SWITCH_N(n, {
-        glsc3_box_kernel<NV><<<red_grid<NV>(E), ColCfg<NV>::THREADS, 0, s>>>(a, b, E, bx, out_dev, rs);
+        glsc3_box_kernel<NV><<<red_grid<NV>(E), PairCfg<NV>::THREADS, 0, s>>>(a, b, E, make_box_flat(bx), out_dev, rs);
         SEM_CHECK_LAUNCH("sem_glsc3_slab launch");
         return 0;
     });
