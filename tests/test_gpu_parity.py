@@ -259,8 +259,14 @@ def test_cg_generic_matches_fused(cuda):
     fused = sb.cg_solve(f, op, topo, sb.CgConfig(25, 0.0))
     generic = sb.cg_solve(f, lambda p: sb.apply_global(p, geom, b, topo), topo,
                           sb.CgConfig(25, 0.0))
-    assert np.array_equal(fused.residual_history, generic.residual_history)
-    assert torch.equal(fused.solution, generic.solution)
+    # same recurrences and kernels; the fused <p,w>_c is accumulated in the
+    # row-mapped assembly kernel, the generic one by glsc3 (flat order), so
+    # the two agree to rounding, each being deterministic on its own
+    h1, h2 = fused.residual_history, generic.residual_history
+    assert np.max(np.abs(h1 - h2) / np.abs(h2)) <= 1e-12
+    assert O.rel_diff(fused.solution.cpu().numpy(), generic.solution.cpu().numpy()) <= 1e-12
+    again = sb.cg_solve(f, op, topo, sb.CgConfig(25, 0.0))
+    assert np.array_equal(again.residual_history, h1)  # run-to-run reproducible
 
 
 def test_cg_e4096_vs_oracle(cuda):
