@@ -269,19 +269,20 @@ static int launch_ax(const double* u, const double* g, const double* dx, double*
 
 constexpr int kAxCarveout = -1;
 
-template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false>
+template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0>
 static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
                          int64_t E, cudaStream_t stream)
 {
     using C = PencilCfg<N>;
     constexpr int THREADS = ((SLOTS * C::NN + 31) / 32) * 32;
-    constexpr size_t SMEM = sizeof(double) * (size_t)SLOTS * C::SLOT_DOUBLES;
+    constexpr size_t SMEM = sizeof(double) * ((size_t)SLOTS * C::SLOT_DOUBLES +
+                                              (GMODE ? (size_t)SLOTS * 6 * C::NNN + 4 : 0));
     static_assert(SMEM * MINB <= 227 * 1024, "pencil kernel shared memory");
     DParamP<N> D;
     for (int c = 0; c < 6; ++c)
         for (int t = 0; t < N * N; ++t) D.d[c][t] = dx[t];
     if (E == 0) return 0;
-    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF>;
+    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE>;
     static bool configured = false;  // per template instance
     if (!configured) {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -308,13 +309,14 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     return 0;
 }
 
-template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false>
+template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0>
 static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
                       cudaStream_t stream)
 {
-    if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 &&
-                  sizeof(double) * SLOTS * PencilCfg<N>::SLOT_DOUBLES * MINB <= 227 * 1024)
-        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF>(u, g, dx, w, E, stream);
+    if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 && (GMODE != 2 || N % 2 == 0) &&
+                  sizeof(double) * ((size_t)SLOTS * PencilCfg<N>::SLOT_DOUBLES +
+                                    (GMODE ? (size_t)SLOTS * 6 * N * N * N + 4 : 0)) * MINB <= 227 * 1024)
+        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE>(u, g, dx, w, E, stream);
     else
         return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false>(u, g, dx, w, E, stream);
 }
@@ -335,6 +337,20 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
     if (variant == 0) variant = kDefaultVariant[N];
     switch (variant) {
         case 19: return try_pencil<N, S, 1, false>(u, g, dx, w, E, stream);
+        case 20: return try_pencil<N, 1, 4, false, 3>(u, g, dx, w, E, stream);
+        case 21: return try_pencil<N, 1, 4, false, 4>(u, g, dx, w, E, stream);
+        case 22: return try_pencil<N, 1, 4, false, 5>(u, g, dx, w, E, stream);
+        case 23: return try_pencil<N, 1, 5, false, 2>(u, g, dx, w, E, stream);
+        case 24: return try_pencil<N, 1, 3, false, 5>(u, g, dx, w, E, stream);
+        case 25: return try_pencil<N, 1, 3, false, 1, false, 1>(u, g, dx, w, E, stream);
+        case 26: return try_pencil<N, 1, 2, false, 1, false, 1>(u, g, dx, w, E, stream);
+        case 27: return try_pencil<N, 1, 3, false, 1, false, 2>(u, g, dx, w, E, stream);
+        case 28: return try_pencil<N, 1, 4, false, 1, false, 1>(u, g, dx, w, E, stream);
+        case 29: return try_pencil<N, 1, 4, false, 1, false, 2>(u, g, dx, w, E, stream);
+        case 30: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 1>(u, g, dx, w, E, stream);
+        case 31: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream);
+        case 32: return try_pencil<N, (S + 2) / 3, 3, false, 1, false, 2>(u, g, dx, w, E, stream);
+        case 33: return try_pencil<N, 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
@@ -398,5 +414,5 @@ extern "C" int sem_ax(const double* u, const double* g, const double* dx,
 
 extern "C" int sem_ax_num_variants(int32_t n)
 {
-    return (n >= 2 && n <= 16) ? 20 : 0;
+    return (n >= 2 && n <= 16) ? 34 : 0;
 }

@@ -80,7 +80,50 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* base, int64_t lo, i
                  : "memory");
 }
 
-template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false>
+// mbarrier + bulk-copy (TMA engine) helpers for the staged-metric mode
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase)
+{
+    asm volatile(
+        "{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        " @!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// GMODE 0: the metric of layers k+1..k+PD is held in a register ring.
+// GMODE 1: the element's whole metric block (48 n^3 B, contiguous) is pulled
+//          into shared memory by ONE bulk copy (TMA engine) at CTA start, so
+//          every byte of g is in flight from the first cycle without costing
+//          registers; S4 reads it with conflict-free LDS.  (SLOTS == 1.)
+// GMODE 2: as 1, and u also arrives by bulk copies (one per k-layer, straight
+//          into the padded U stack) on its own mbarrier, so S3 starts as soon
+//          as u lands while g is still streaming.
+template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false,
+          int GMODE = 0>
 __global__ void __launch_bounds__(THREADS, MINB)
 ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                  double* __restrict__ w, int64_t num_elements, const DParamP<N> D,
@@ -98,6 +141,13 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     double* U = smem + (size_t)sl * C::SLOT_DOUBLES;
     double* A = U + N * LSU;
     double* B = A + N * LSA;
+    // GMODE >= 1: per-slot staged metric blocks after the slot stacks, then
+    // the two mbarriers (u, g) shared by the CTA
+    double* Gbase = smem + (size_t)SLOTS * C::SLOT_DOUBLES;
+    double* G = Gbase + (size_t)sl * 6 * NNN;
+    uint64_t* gbar = reinterpret_cast<uint64_t*>(Gbase + (GMODE ? (size_t)SLOTS * 6 * NNN : 0));
+    uint64_t* ubar = gbar + 1;
+    static_assert(GMODE == 0 || !PERSIST, "staged metric: one batch per CTA");
 
     // index maps of the three pencil families (see header comment)
     const int kp_i = p % N, kp_j = p / N;          // k-pencil (i,j): p = j*N + i
@@ -118,19 +168,47 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
 #pragma unroll
         for (int k = 0; k < N; ++k) ucol[k] = ok ? __ldg(src + k * NN) : 0.0;
     };
-    load_ucol(batch);
+    if constexpr (GMODE != 2) load_ucol(batch);
 
     for (; batch < nbatches; batch += (PERSIST ? gridDim.x : nbatches)) {
         const int64_t e = batch * SLOTS + slot;
         const bool active = lane_ok && e < num_elements;
         const double* ge = g + (active ? e : 0) * (6 * NNN) + p;  // k-pencil point (i,j)
         // metric of layers 0..PD-1: issued first, in flight during S3/S1/S2
-        double gq[PD][6];
+        double gq[GMODE ? 1 : PD][6];
+        if constexpr (GMODE >= 1) {
+            if (tid == 0) {
+                mbar_init(gbar, 1);
+                if (GMODE == 2) mbar_init(ubar, 1);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                const int64_t e0 = batch * SLOTS;
+                const int nact = (int)((num_elements - e0) < SLOTS ? (num_elements - e0) : SLOTS);
+                if constexpr (GMODE == 2) {
+                    mbar_expect_tx(ubar, (unsigned)(nact * NNN * 8));
+                    for (int s2 = 0; s2 < nact; ++s2)
+                        for (int k = 0; k < N; ++k)
+                            bulk_g2s(smem + (size_t)s2 * C::SLOT_DOUBLES + k * LSU,
+                                     u + (e0 + s2) * NNN + k * NN, NN * 8, ubar);
+                }
+                mbar_expect_tx(gbar, (unsigned)(nact * 6 * NNN * 8));
+                for (int s2 = 0; s2 < nact; ++s2)
+                    bulk_g2s(Gbase + (size_t)s2 * 6 * NNN, g + (e0 + s2) * (6 * NNN),
+                             6 * NNN * 8, gbar);
+            }
+            if constexpr (GMODE == 2) {
+                mbar_wait(ubar, 0);
 #pragma unroll
-        for (int d = 0; d < PD; ++d)
+                for (int k = 0; k < N; ++k) ucol[k] = active ? U[k * LSU + p] : 0.0;
+            }
+        } else {
 #pragma unroll
-            for (int m = 0; m < 6; ++m)
-                gq[d][m] = (active && d < N) ? __ldg(ge + m * NNN + d * NN) : 0.0;
+            for (int d = 0; d < PD; ++d)
+#pragma unroll
+                for (int m = 0; m < 6; ++m)
+                    gq[d][m] = (active && d < N) ? __ldg(ge + m * NNN + d * NN) : 0.0;
+        }
         // warm L2 with the element this slot will process pf_elems later
         if (L2PF && pf_elems > 0 && lane_ok && p == 0 && e + pf_elems < num_elements) {
             const int64_t en = e + pf_elems;
@@ -143,7 +221,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         double wt[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            if (lane_ok) U[k * LSU + p] = ucol[k];
+            if (GMODE != 2 && lane_ok) U[k * LSU + p] = ucol[k];
             double s = 0.0;
 #pragma unroll
             for (int l = 0; l < N; ++l) s = fma(D.d[kStS3][k * N + l], ucol[l], s);
@@ -202,19 +280,25 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         __syncthreads();
 
         // ---- S4: k-pencil metric per layer; ut scattered into Wt ----------
+        if constexpr (GMODE >= 1) mbar_wait(gbar, 0);
         double Wt[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) Wt[k] = 0.0;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            // register ring: consume layer k, refill the slot with layer k+PD
             double gc[6];
+            if constexpr (GMODE >= 1) {
 #pragma unroll
-            for (int m = 0; m < 6; ++m) gc[m] = gq[k % PD][m];
-            if (k + PD < N) {
+                for (int m = 0; m < 6; ++m) gc[m] = G[m * NNN + k * NN + p];
+            } else {
+                // register ring: consume layer k, refill the slot with layer k+PD
 #pragma unroll
-                for (int m = 0; m < 6; ++m)
-                    gq[k % PD][m] = active ? __ldg(ge + m * NNN + (k + PD) * NN) : 0.0;
+                for (int m = 0; m < 6; ++m) gc[m] = gq[k % PD][m];
+                if (k + PD < N) {
+#pragma unroll
+                    for (int m = 0; m < 6; ++m)
+                        gq[k % PD][m] = active ? __ldg(ge + m * NNN + (k + PD) * NN) : 0.0;
+                }
             }
             if (lane_ok) {
                 const double a = A[k * LSA + p];
@@ -278,7 +362,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             }
         }
         // next batch's u columns: in flight across the barrier and S7
-        if (PERSIST) load_ucol(batch + gridDim.x);
+        if (PERSIST && GMODE != 2) load_ucol(batch + gridDim.x);
         __syncthreads();
 
         // ---- S7: k-pencil: w = A + B + Wt ----------------------------------
