@@ -276,7 +276,7 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     using C = PencilCfg<N>;
     constexpr int THREADS = ((SLOTS * C::NN + 31) / 32) * 32;
     constexpr size_t SMEM = sizeof(double) * ((size_t)SLOTS * C::SLOT_DOUBLES +
-                                              (GMODE ? (size_t)SLOTS * 6 * C::NNN + 4 : 0));
+                                              (GMODE ? (size_t)SLOTS * 6 * C::NNN + 6 : 0));
     static_assert(SMEM * MINB <= 227 * 1024, "pencil kernel shared memory");
     DParamP<N> D;
     for (int c = 0; c < 6; ++c)
@@ -315,7 +315,7 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 {
     if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 && (GMODE != 2 || N % 2 == 0) &&
                   sizeof(double) * ((size_t)SLOTS * PencilCfg<N>::SLOT_DOUBLES +
-                                    (GMODE ? (size_t)SLOTS * 6 * N * N * N + 4 : 0)) * MINB <= 227 * 1024)
+                                    (GMODE ? (size_t)SLOTS * 6 * N * N * N + 6 : 0)) * MINB <= 227 * 1024)
         return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE>(u, g, dx, w, E, stream);
     else
         return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false>(u, g, dx, w, E, stream);
@@ -327,7 +327,7 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 // prefetch depth, persistent, L2 bulk prefetch>.
 // Default tuning point per n (tools/ax_sweep.py on B200, E=4096; see
 // profiles/r01_ax_sweep.txt, CUDA-graph timed): index = n, value = variant id.
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 19, 16, 15, 16, 9, 13, 15, 9, 5, 8, 7, 17, 3};
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 26, 26, 28, 26, 26, 25, 26, 5, 8, 7, 17, 3};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,

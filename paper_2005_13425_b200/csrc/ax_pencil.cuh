@@ -143,7 +143,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     double* B = A + N * LSA;
     // GMODE >= 1: per-slot staged metric blocks after the slot stacks, then
     // the two mbarriers (u, g) shared by the CTA
-    double* Gbase = smem + (size_t)SLOTS * C::SLOT_DOUBLES;
+    double* Gbase = smem + ((size_t)SLOTS * C::SLOT_DOUBLES + 1) / 2 * 2;  // 16-B aligned
     double* G = Gbase + (size_t)sl * 6 * NNN;
     uint64_t* gbar = reinterpret_cast<uint64_t*>(Gbase + (GMODE ? (size_t)SLOTS * 6 * NNN : 0));
     uint64_t* ubar = gbar + 1;
