@@ -21,6 +21,7 @@
 //
 // Arithmetic differs from the reference only by FMA contraction and
 // association (tolerance 1e-12 max-norm relative, sembench/verify.py:37-42).
+#include <math.h>
 #include <stdlib.h>
 
 #include "sem_common.cuh"
@@ -269,7 +270,40 @@ static int launch_ax(const double* u, const double* g, const double* dx, double*
 
 constexpr int kAxCarveout = -1;
 
-template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0>
+// Kernel-parameter D tables (one copy per stage) and their even-odd forms.
+// Returns whether D is centro-antisymmetric to 1e-13 relative, i.e. whether
+// the folded contraction is usable (it is for every GLL basis).
+template <int N>
+static bool fill_dparam(DParamP<N>& P, const double* dx)
+{
+    constexpr int H = N / 2, c = (N - 1) / 2;
+    double dev = 0.0, scale = 0.0;
+    for (int i = 0; i < N; ++i)
+        for (int l = 0; l < N; ++l) {
+            const double v = dx[i * N + l];
+            scale = fabs(v) > scale ? fabs(v) : scale;
+            const double d = fabs(dx[(N - 1 - i) * N + (N - 1 - l)] + v);
+            dev = d > dev ? d : dev;
+        }
+    for (int st = 0; st < 6; ++st) {
+        for (int t = 0; t < N * N; ++t) P.d[st][t] = dx[t];
+        const bool trans = (st == kStS4 || st == kStS5 || st == kStS6);
+        auto M = [&](int i, int l) { return trans ? dx[l * N + i] : dx[i * N + l]; };
+        for (int i = 0; i < H; ++i)
+            for (int l = 0; l < H; ++l) {
+                P.a[st][i * H + l] = 0.5 * (M(i, l) + M(i, N - 1 - l));
+                P.b[st][i * H + l] = 0.5 * (M(i, l) - M(i, N - 1 - l));
+            }
+        if (N % 2 == 1) {
+            for (int i = 0; i < H; ++i) P.mc[st][i] = M(i, c);
+            for (int l = 0; l < H; ++l) P.mr[st][l] = 0.5 * (M(c, l) - M(c, N - 1 - l));
+        }
+    }
+    return dev <= 1e-13 * scale;
+}
+
+template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
+          bool FOLD = false>
 static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
                          int64_t E, cudaStream_t stream)
 {
@@ -279,10 +313,14 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
                                               (GMODE ? (size_t)SLOTS * 6 * C::NNN + 6 : 0));
     static_assert(SMEM * MINB <= 227 * 1024, "pencil kernel shared memory");
     DParamP<N> D;
-    for (int c = 0; c < 6; ++c)
-        for (int t = 0; t < N * N; ++t) D.d[c][t] = dx[t];
+    const bool antisym = fill_dparam<N>(D, dx);
+    if constexpr (FOLD) {
+        if (!antisym)  // the even-odd form needs a centro-antisymmetric D
+            return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, false>(u, g, dx, w, E,
+                                                                               stream);
+    }
     if (E == 0) return 0;
-    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE>;
+    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE, FOLD>;
     static bool configured = false;  // per template instance
     if (!configured) {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -309,14 +347,16 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     return 0;
 }
 
-template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0>
+template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
+          bool FOLD = false>
 static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
                       cudaStream_t stream)
 {
     if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 && (GMODE != 2 || N % 2 == 0) &&
                   sizeof(double) * ((size_t)SLOTS * PencilCfg<N>::SLOT_DOUBLES +
                                     (GMODE ? (size_t)SLOTS * 6 * N * N * N + 6 : 0)) * MINB <= 227 * 1024)
-        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE>(u, g, dx, w, E, stream);
+        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD>(u, g, dx, w, E,
+                                                                          stream);
     else
         return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false>(u, g, dx, w, E, stream);
 }
@@ -351,6 +391,13 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
         case 31: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream);
         case 32: return try_pencil<N, (S + 2) / 3, 3, false, 1, false, 2>(u, g, dx, w, E, stream);
         case 33: return try_pencil<N, 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream);
+        // even-odd folded contractions (centro-antisymmetric D only)
+        case 34: return try_pencil<N, 1, 3, false, 1, false, 1, true>(u, g, dx, w, E, stream);
+        case 35: return try_pencil<N, 1, 2, false, 1, false, 1, true>(u, g, dx, w, E, stream);
+        case 36: return try_pencil<N, 1, 5, false, 3, false, 0, true>(u, g, dx, w, E, stream);
+        case 37: return try_pencil<N, 1, 4, false, 1, false, 1, true>(u, g, dx, w, E, stream);
+        case 38: return try_pencil<N, 1, 3, false, 1, false, 2, true>(u, g, dx, w, E, stream);
+        case 39: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 1, true>(u, g, dx, w, E, stream);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
@@ -414,5 +461,5 @@ extern "C" int sem_ax(const double* u, const double* g, const double* dx,
 
 extern "C" int sem_ax_num_variants(int32_t n)
 {
-    return (n >= 2 && n <= 16) ? 34 : 0;
+    return (n >= 2 && n <= 16) ? 40 : 0;
 }

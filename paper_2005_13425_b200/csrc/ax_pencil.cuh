@@ -60,8 +60,65 @@ constexpr int kStS3 = 0, kStS1 = 1, kStS2 = 2, kStS4 = 3, kStS5 = 4, kStS6 = 5;
 
 template <int N>
 struct DParamP {
+    static constexpr int H = N / 2;
     double d[6][N * N];
+    // even-odd ("fold") form of the stage matrix M (M = D for S3/S1/S2,
+    // M = D^T for S4/S5/S6), valid when M is centro-antisymmetric
+    // (M[n-1-i][n-1-l] = -M[i][l], true of every GLL derivative matrix):
+    //   a[i][l] = (M[i][l] + M[i][n-1-l]) / 2,  b[i][l] = (M[i][l] - M[i][n-1-l]) / 2
+    //   mc[i] = M[i][c], mr[l] = (M[c][l] - M[c][n-1-l]) / 2   (odd n, c = (n-1)/2)
+    double a[6][H * H > 0 ? H * H : 1];
+    double b[6][H * H > 0 ? H * H : 1];
+    double mc[6][H > 0 ? H : 1];
+    double mr[6][H > 0 ? H : 1];
 };
+
+// out = M in for one pencil.  FOLD uses the even-odd form: with e = in_l +
+// in_{n-1-l}, o = in_l - in_{n-1-l}, S_i = a e (+ mc in_c), T_i = b o:
+// out_i = S_i + T_i, out_{n-1-i} = T_i - S_i -- n^2/2 FMAs + 2n adds instead
+// of n^2 FMAs (fewer FP64 and constant-load instructions per point).
+template <int N, bool FOLD, bool TRANS>
+__device__ __forceinline__ void pencil_gemv(const DParamP<N>& D, int st, const double (&in)[N],
+                                            double (&out)[N])
+{
+    if constexpr (!FOLD) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < N; ++l)
+                s = fma(TRANS ? D.d[st][l * N + i] : D.d[st][i * N + l], in[l], s);
+            out[i] = s;
+        }
+    } else {
+        constexpr int H = N / 2;
+        constexpr int c = (N - 1) / 2;
+        double e[H > 0 ? H : 1], o[H > 0 ? H : 1];
+#pragma unroll
+        for (int l = 0; l < H; ++l) {
+            e[l] = in[l] + in[N - 1 - l];
+            o[l] = in[l] - in[N - 1 - l];
+        }
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            double S = 0.0, T = 0.0;
+#pragma unroll
+            for (int l = 0; l < H; ++l) {
+                S = fma(D.a[st][i * H + l], e[l], S);
+                T = fma(D.b[st][i * H + l], o[l], T);
+            }
+            if constexpr (N % 2 == 1) S = fma(D.mc[st][i], in[c], S);
+            out[i] = S + T;
+            out[N - 1 - i] = T - S;
+        }
+        if constexpr (N % 2 == 1) {
+            double T = 0.0;
+#pragma unroll
+            for (int l = 0; l < H; ++l) T = fma(D.mr[st][l], o[l], T);
+            out[c] = T;
+        }
+    }
+}
 
 // Bulk L2 prefetch (sm_90+ cp.async.bulk.prefetch.L2): one instruction
 // pulls a whole element's u or g block from HBM into L2, so the demand
@@ -123,7 +180,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase)
 //          into the padded U stack) on its own mbarrier, so S3 starts as soon
 //          as u lands while g is still streaming.
 template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false,
-          int GMODE = 0>
+          int GMODE = 0, bool FOLD = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                  double* __restrict__ w, int64_t num_elements, const DParamP<N> D,
@@ -220,13 +277,9 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         // ---- S3: k-pencil -- stage u, wt = D u_col -------------------------
         double wt[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
+        for (int k = 0; k < N; ++k)
             if (GMODE != 2 && lane_ok) U[k * LSU + p] = ucol[k];
-            double s = 0.0;
-#pragma unroll
-            for (int l = 0; l < N; ++l) s = fma(D.d[kStS3][k * N + l], ucol[l], s);
-            wt[k] = s;
-        }
+        pencil_gemv<N, FOLD, false>(D, kStS3, ucol, wt);
         __syncthreads();
 
         // ---- S1: i-pencil (j,k): wr[i] = sum_l D[i][l] U[k][j][l] ----------
@@ -245,13 +298,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                 for (int l = 0; l < N; ++l) row[l] = src[l];
             }
             double out[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int l = 0; l < N; ++l) s = fma(D.d[kStS1][i * N + l], row[l], s);
-                out[i] = s;
-            }
+            pencil_gemv<N, FOLD, false>(D, kStS1, row, out);
             double* dst = A + ip_k * LSA + ip_j * N;
             if (C::VEC) {
 #pragma unroll
@@ -269,19 +316,16 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
 #pragma unroll
             for (int l = 0; l < N; ++l) col[l] = src[l * N];
             double* dst = B + jp_k * LSB + jp_i;
+            double out[N];
+            pencil_gemv<N, FOLD, false>(D, kStS2, col, out);
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-#pragma unroll
-                for (int l = 0; l < N; ++l) s = fma(D.d[kStS2][j * N + l], col[l], s);
-                dst[j * N] = s;
-            }
+            for (int j = 0; j < N; ++j) dst[j * N] = out[j];
         }
         __syncthreads();
 
         // ---- S4: k-pencil metric per layer; ut scattered into Wt ----------
         if constexpr (GMODE >= 1) mbar_wait(gbar, 0);
-        double Wt[N];
+        double Wt[N], utk[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) Wt[k] = 0.0;
 #pragma unroll
@@ -309,10 +353,18 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                 const double ut = fma(gc[5], t, fma(gc[4], b, gc[2] * a));
                 A[k * LSA + p] = ur;
                 B[k * LSB + p] = us;
+                if constexpr (FOLD) {
+                    utk[k] = ut;  // folded D^T applied once all layers are known
+                } else {
 #pragma unroll
-                for (int kk = 0; kk < N; ++kk) Wt[kk] = fma(D.d[kStS4][k * N + kk], ut, Wt[kk]);
+                    for (int kk = 0; kk < N; ++kk)
+                        Wt[kk] = fma(D.d[kStS4][k * N + kk], ut, Wt[kk]);
+                }
+            } else if constexpr (FOLD) {
+                utk[k] = 0.0;
             }
         }
+        if constexpr (FOLD) pencil_gemv<N, true, true>(D, kStS4, utk, Wt);
         __syncthreads();
 
         // ---- S5: i-pencil: A row <- D^T A row ------------------------------
@@ -331,13 +383,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                 for (int l = 0; l < N; ++l) row[l] = rp[l];
             }
             double out[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int l = 0; l < N; ++l) s = fma(D.d[kStS5][l * N + i], row[l], s);
-                out[i] = s;
-            }
+            pencil_gemv<N, FOLD, true>(D, kStS5, row, out);
             if (C::VEC) {
 #pragma unroll
                 for (int q = 0; q < N / 2; ++q)
@@ -353,13 +399,10 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             double* cp = B + jp_k * LSB + jp_i;
 #pragma unroll
             for (int l = 0; l < N; ++l) col[l] = cp[l * N];
+            double out[N];
+            pencil_gemv<N, FOLD, true>(D, kStS6, col, out);
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-#pragma unroll
-                for (int l = 0; l < N; ++l) s = fma(D.d[kStS6][l * N + j], col[l], s);
-                cp[j * N] = s;
-            }
+            for (int j = 0; j < N; ++j) cp[j * N] = out[j];
         }
         // next batch's u columns: in flight across the barrier and S7
         if (PERSIST && GMODE != 2) load_ucol(batch + gridDim.x);
