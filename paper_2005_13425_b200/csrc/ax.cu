@@ -367,7 +367,7 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 // prefetch depth, persistent, L2 bulk prefetch>.
 // Default tuning point per n (tools/ax_sweep.py on B200, E=4096; see
 // profiles/r01_ax_sweep.txt, CUDA-graph timed): index = n, value = variant id.
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 26, 26, 28, 26, 26, 25, 26, 5, 8, 7, 17, 3};
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 37, 34, 34, 35, 5, 8, 7, 17, 3};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,

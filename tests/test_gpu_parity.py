@@ -124,6 +124,19 @@ def test_ax_host_streaming(cuda, kind):
     assert torch.equal(out_t, dev_out)
 
 
+@pytest.mark.parametrize("n", [5, 10, 11])
+def test_ax_general_D_not_folded(cuda, n):
+    """The even-odd fold is used only for a centro-antisymmetric D (every GLL
+    basis); an arbitrary D must take the exact path and still match."""
+    E = 9
+    u, g = _rand_inputs(E, n, 31 + n, 41 + n)
+    D = O.random_field(1, n, 7).reshape(-1)[: n * n].reshape(n, n).copy()
+    b = sb.PolynomialBasis(n=n, nodes=np.zeros(n), weights=np.ones(n), diff=D,
+                           diff_t=D.T.copy())
+    w = sb.apply_ax(u, sb.GeomFactors(values=g), b)
+    assert O.rel_diff(w, O.ax_layered(u, g, D, D.T.copy())) <= AX_TOL
+
+
 def test_ax_does_not_mutate_and_empty(cuda):
     b = sb.build_basis(6)
     u, g = _rand_inputs(3, 6, 5, 6)
