@@ -34,6 +34,7 @@ __all__ = ["CgConfig", "CgResult", "CgBreakdownError", "weighted_dot", "cg_solve
            "CG_VECTOR_FLOPS_PER_POINT", "CgWorkspace"]
 
 CG_VECTOR_FLOPS_PER_POINT = 12
+USE_GRAPHS = True  # replay one captured iteration (fused path)
 
 
 class CgBreakdownError(RuntimeError):
@@ -97,6 +98,23 @@ class CgWorkspace:
                                    device=device)
         self.device = device
         self.max_iterations = max_iterations
+        self._graph = None
+        self._graph_key = None
+
+    def iteration_graph(self, launch_one, key):
+        """CUDA graph of one fused iteration (captured once per workspace and
+        operator: `key` identifies the captured geometry / basis / box)."""
+        if self._graph is None or self._graph_key != key:
+            self._graph_key = key
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    launch_one()
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            self._graph = g
+        return self._graph
 
     def read_state(self) -> sem_cg_state:
         raw = self.state.cpu().numpy().tobytes()
@@ -129,7 +147,18 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
                              dv.ptr(ws.history), k, *box, dv.ptr(ws.scratch), s), "cg_solve run")
 
     if callback is None:
-        run(cfg.max_iterations)
+        if cfg.max_iterations > 2 and USE_GRAPHS:
+            # iteration 1 launched directly (configures the kernels), then one
+            # iteration is captured into a CUDA graph and replayed: the
+            # iteration's launches are parameter-stable (scalars live in the
+            # device state), so replay == relaunch without the host overhead
+            run(1)
+            key = (g.data_ptr(), box, dx.tobytes())
+            graph = ws.iteration_graph(lambda: run(1), key)
+            for _ in range(cfg.max_iterations - 1):
+                graph.replay()
+        else:
+            run(cfg.max_iterations)
         st = ws.read_state()
     else:
         st = None
