@@ -172,6 +172,11 @@ int sem_cg_init_slab(const double *f, double *x, double *r, double *p, sem_cg_st
                      void *scratch, sem_stream_t stream);
 int sem_cg_p(double *p, const double *r, int64_t m, sem_cg_state *state, double *history,
              sem_stream_t stream);
+/* Iteration head fused with the operator: exact-zero exit / beta / p = beta*p + r
+ * (cg.py:149-160) in the Ax prologue, then w = A_local p (one launch). */
+int sem_cg_ax(double *p, const double *r, const double *g, const double *dx, const double *dxt,
+              double *w, int64_t num_elements, int32_t n, sem_cg_state *state,
+              double *history, sem_stream_t stream);
 int sem_cg_assemble_slab(const double *w, double *w2, const double *p,
                          const double *bottom_totals, const double *top_totals,
                          sem_cg_state *state, int32_t ex, int32_t ey, int32_t ez, int32_t n,

@@ -26,6 +26,7 @@
 
 #include "sem_common.cuh"
 #include "ax_pencil.cuh"
+#include "box.cuh"
 
 namespace sem {
 
@@ -303,9 +304,9 @@ static bool fill_dparam(DParamP<N>& P, const double* dx)
 }
 
 template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
-          bool FOLD = false>
+          bool FOLD = false, bool CGP = false>
 static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
-                         int64_t E, cudaStream_t stream)
+                         int64_t E, cudaStream_t stream, CgpArgs cgp = CgpArgs{})
 {
     using C = PencilCfg<N>;
     constexpr int THREADS = ((SLOTS * C::NN + 31) / 32) * 32;
@@ -316,11 +317,11 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     const bool antisym = fill_dparam<N>(D, dx);
     if constexpr (FOLD) {
         if (!antisym)  // the even-odd form needs a centro-antisymmetric D
-            return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, false>(u, g, dx, w, E,
-                                                                               stream);
+            return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, false, CGP>(
+                u, g, dx, w, E, stream, cgp);
     }
     if (E == 0) return 0;
-    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE, FOLD>;
+    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGP>;
     static bool configured = false;  // per template instance
     if (!configured) {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -342,23 +343,24 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     const int64_t grid = PERSIST ? (nbatches < resident ? nbatches : resident) : nbatches;
     // prefetch distance: the batch that replaces this one on its SM
     const int64_t pf = (nbatches > resident) ? resident * SLOTS : 0;
-    kern<<<(unsigned)grid, THREADS, SMEM, stream>>>(u, g, w, E, D, pf);
+    kern<<<(unsigned)grid, THREADS, SMEM, stream>>>(u, g, w, E, D, pf, cgp);
     SEM_CHECK_LAUNCH("sem_ax (pencil) launch");
     return 0;
 }
 
 template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
-          bool FOLD = false>
+          bool FOLD = false, bool CGP = false>
 static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
-                      cudaStream_t stream)
+                      cudaStream_t stream, CgpArgs cgp = CgpArgs{})
 {
     if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 && (GMODE != 2 || N % 2 == 0) &&
                   sizeof(double) * ((size_t)SLOTS * PencilCfg<N>::SLOT_DOUBLES +
                                     (GMODE ? (size_t)SLOTS * 6 * N * N * N + 6 : 0)) * MINB <= 227 * 1024)
-        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD>(u, g, dx, w, E,
-                                                                          stream);
+        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGP>(u, g, dx, w, E,
+                                                                               stream, cgp);
     else
-        return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false>(u, g, dx, w, E, stream);
+        return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, CGP>(
+            u, g, dx, w, E, stream, cgp);
 }
 
 // variant 0: the tuned default for this n (kDefaultVariant);
@@ -419,6 +421,30 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
             set_error("sem_ax: unknown variant %d", variant);
             return SEM_E_INVALID;
     }
+}
+
+// CG iteration head fused with Ax (p = beta p + r; w = A_local p): the tuned
+// configuration of each n with the metric staged by TMA and u through
+// registers (the p update happens while the column is loaded).
+template <int N>
+static int ax_cg_n(double* p, const double* r, const double* g, const double* dx, double* w,
+                   int64_t E, sem_cg_state* st, double* hist, cudaStream_t s)
+{
+    const CgpArgs a{p, r, st, hist};
+    if constexpr (N >= 5 && N <= 11)
+        return try_pencil<N, 1, 3, false, 1, false, 1, true, true>(p, g, dx, w, E, s, a);
+    else if constexpr (N == 4)
+        return try_pencil<N, 1, 2, false, 1, false, 1, false, true>(p, g, dx, w, E, s, a);
+    else
+        return try_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, true>(p, g, dx, w,
+                                                                                    E, s, a);
+}
+
+int ax_cg_dispatch(double* p, const double* r, const double* g, const double* dx, double* w,
+                   int64_t E, int n, sem_cg_state* st, double* hist, cudaStream_t stream)
+{
+    if (E == 0) return 0;
+    SEM_SWITCH_N(n, return ax_cg_n<NV>(p, r, g, dx, w, E, st, hist, stream));
 }
 
 int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,

@@ -179,12 +179,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase)
 // GMODE 2: as 1, and u also arrives by bulk copies (one per k-layer, straight
 //          into the padded U stack) on its own mbarrier, so S3 starts as soon
 //          as u lands while g is still streaming.
+// CG fusion (CGP): the top of a CG iteration (sembench/cg.py:149-160:
+// exact-zero exit, beta = rtz/rtz_old, p = beta*p + r, unfused multiply-add)
+// is folded into the Ax prologue: the kernel reads p_old and r, writes p_new
+// back and applies the operator to it -- one pass over p fewer per iteration.
+struct CgpArgs {
+    double* p;            // p (read old, write new)
+    const double* r;
+    sem_cg_state* st;
+    double* history;
+};
+
 template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false,
-          int GMODE = 0, bool FOLD = false>
+          int GMODE = 0, bool FOLD = false, bool CGP = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                  double* __restrict__ w, int64_t num_elements, const DParamP<N> D,
-                 int64_t pf_elems)
+                 int64_t pf_elems, CgpArgs cgp)
 {
     using C = PencilCfg<N>;
     constexpr int NN = C::NN, NNN = C::NNN, LSU = C::LSU, LSA = C::LSA, LSB = C::LSB;
@@ -217,13 +228,43 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     // otherwise one batch per CTA (D constants are not loop-invariant, so
     // the compiler keeps them in uniform registers only around their use).
 
+    double beta = 0.0;
+    if constexpr (CGP) {
+        static_assert(!PERSIST && GMODE != 2, "CG fusion: one batch per CTA, u via registers");
+        sem_cg_state* st = cgp.st;
+        if (st->stop) return;                       // uniform over the grid
+        const int it = st->it + 1;
+        const double rtz = st->rtz;
+        if (rtz == 0.0) {                            // cg.py:151-158
+            if (blockIdx.x == 0 && tid == 0) {
+                cgp.history[it - 1] = 0.0;
+                st->iterations_run = it;
+                st->stop = 1;
+            }
+            return;
+        }
+        beta = (it == 1) ? 0.0 : rtz / st->rtz_old;
+        if (blockIdx.x == 0 && tid == 0) st->beta = beta;
+    }
     double ucol[N];
     auto load_ucol = [&](int64_t b) {
         const int64_t e = b * SLOTS + slot;
         const bool ok = lane_ok && b < nbatches && e < num_elements;
-        const double* src = u + (ok ? e : 0) * NNN + kp_j * N + kp_i;
+        if constexpr (CGP) {
+            double* pp = cgp.p + (ok ? e : 0) * NNN + kp_j * N + kp_i;
+            const double* rp = cgp.r + (ok ? e : 0) * NNN + kp_j * N + kp_i;
 #pragma unroll
-        for (int k = 0; k < N; ++k) ucol[k] = ok ? __ldg(src + k * NN) : 0.0;
+            for (int k = 0; k < N; ++k)
+                ucol[k] = ok ? add_rn(mul_rn(beta, pp[k * NN]), __ldg(rp + k * NN)) : 0.0;
+            if (ok) {
+#pragma unroll
+                for (int k = 0; k < N; ++k) pp[k * NN] = ucol[k];
+            }
+        } else {
+            const double* src = u + (ok ? e : 0) * NNN + kp_j * N + kp_i;
+#pragma unroll
+            for (int k = 0; k < N; ++k) ucol[k] = ok ? __ldg(src + k * NN) : 0.0;
+        }
     };
     if constexpr (GMODE != 2) load_ucol(batch);
 

@@ -24,6 +24,8 @@ namespace sem {
 
 int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
                 int n, int variant, cudaStream_t stream);
+int ax_cg_dispatch(double* p, const double* r, const double* g, const double* dx, double* w,
+                   int64_t E, int n, sem_cg_state* st, double* hist, cudaStream_t stream);
 
 constexpr int kVecThreads = 256;
 
@@ -103,7 +105,7 @@ glsc3_box_kernel(const double* __restrict__ a, const double* __restrict__ b, int
 // Scalar bookkeeping of the three reductions of an iteration, shared by the
 // single-GPU kernels (total = this GPU's sum) and the multi-GPU finish kernel
 // (total = per-rank partials combined in rank order).
-constexpr int kPhaseInit = 0, kPhasePap = 1, kPhaseRr = 2;
+constexpr int kPhaseInit = 0, kPhasePap = 1;  // 2 = <r,r> (fin_rr)
 
 __device__ __forceinline__ void fin_init(sem_cg_state* st, double rtz)
 {
@@ -311,12 +313,9 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
                     double* w, double* w2, sem_cg_state* st, double* history, int iters,
                     int64_t E, Box bx, ReduceScratch* rs, cudaStream_t s)
 {
-    constexpr int NNN = N * N * N;
-    const int64_t m = E * NNN;
     for (int it = 0; it < iters; ++it) {
-        cg_p_kernel<<<vec_grid(m), kVecThreads, 0, s>>>(p, r, m, st, history);
-        SEM_CHECK_LAUNCH("cg_p_kernel");
-        if (int rc = ax_dispatch(p, g, dx, w, E, N, 0, s)) return rc;
+        // p = beta p + r fused into the Ax prologue (ax_pencil.cuh, CGP)
+        if (int rc = ax_cg_dispatch(p, r, g, dx, w, E, N, st, history, s)) return rc;
         cg_assemble_kernel<N, false><<<row_grid<N>(E), kRowThreads, 0, s>>>(w, w2, p, E, bx, st,
                                                                              rs, nullptr, nullptr);
         SEM_CHECK_LAUNCH("cg_assemble_kernel");
@@ -504,6 +503,20 @@ extern "C" int sem_cg_p(double* p, const double* r, int64_t m, sem_cg_state* sta
     cg_p_kernel<<<vec_grid(m), kVecThreads, 0, s>>>(p, r, m, state, history);
     SEM_CHECK_LAUNCH("sem_cg_p launch");
     return 0;
+}
+
+extern "C" int sem_cg_ax(double* p, const double* r, const double* g, const double* dx,
+                         const double* dxt, double* w, int64_t num_elements, int32_t n,
+                         sem_cg_state* state, double* history, sem_stream_t stream)
+{
+    if (!p || !r || !g || !dx || !dxt || !w || !state || !history || num_elements < 0 ||
+        n < 2 || n > 16) {
+        set_error("sem_cg_ax: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    return ax_cg_dispatch(p, r, g, dx, w, num_elements, n, state, history, s);
 }
 
 extern "C" int sem_cg_assemble_slab(const double* w, double* w2, const double* p,

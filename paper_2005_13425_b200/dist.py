@@ -204,14 +204,14 @@ class CudaSlabOps:
                                      phase, dv.ptr(self.history), self._s()), "dist cg finish")
 
     def p_update(self) -> None:
-        check(self.lib.sem_cg_p(dv.ptr(self.p), dv.ptr(self.r), self.p.numel(),
-                                dv.ptr(self.state), dv.ptr(self.history), self._s()), "cg p")
+        """p = beta p + r is fused into the Ax launch (sem_cg_ax) below."""
 
     def ax(self) -> None:
         p = self.part
-        check(self.lib.sem_ax(dv.ptr(self.p), dv.ptr(self.g), dv.host_f64_ptr(self.dx),
-                              dv.host_f64_ptr(self.dxt), dv.ptr(self.w), p.num_elements, p.n,
-                              self._s()), "dist cg ax")
+        check(self.lib.sem_cg_ax(dv.ptr(self.p), dv.ptr(self.r), dv.ptr(self.g),
+                                 dv.host_f64_ptr(self.dx), dv.host_f64_ptr(self.dxt),
+                                 dv.ptr(self.w), p.num_elements, p.n, dv.ptr(self.state),
+                                 dv.ptr(self.history), self._s()), "dist cg ax")
 
     def plane_top(self, field: torch.Tensor) -> torch.Tensor:
         p = self.part
