@@ -142,9 +142,11 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
                           float(cfg.tolerance), *box, dv.ptr(ws.scratch), s), "cg_solve init")
 
     def run(k: int):
+        # stream looked up at call time: inside graph capture it is the capture stream
         check(lib.sem_cg_run(dv.ptr(g), dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt), dv.ptr(ws.x),
                              dv.ptr(ws.r), dv.ptr(ws.p), dv.ptr(ws.w), dv.ptr(ws.state),
-                             dv.ptr(ws.history), k, *box, dv.ptr(ws.scratch), s), "cg_solve run")
+                             dv.ptr(ws.history), k, *box, dv.ptr(ws.scratch),
+                             dv.stream_handle(dev)), "cg_solve run")
 
     if callback is None:
         if cfg.max_iterations > 2 and USE_GRAPHS:

@@ -266,6 +266,23 @@ def test_cg_fused_vs_golden(cuda, golden, key):
         assert O.rel_diff(res.solution.cpu().numpy(), golden[f"cg/{key}/solution"]) <= tol
 
 
+def test_cg_graph_replay_matches_eager(cuda):
+    """The fused solver replays one captured CUDA-graph iteration; it must
+    equal eager launching bit for bit."""
+    from paper_2005_13425_b200 import cg as C
+    b, topo, geom, f = _cg_problem(2, 2, 2, 6)
+    op = sb.GlobalOperator(geom, b, topo)
+    C.USE_GRAPHS = False
+    try:
+        eager = sb.cg_solve(f, op, topo, sb.CgConfig(30, 0.0))
+    finally:
+        C.USE_GRAPHS = True
+    graph = sb.cg_solve(f, op, topo, sb.CgConfig(30, 0.0))
+    assert graph.iterations_run == eager.iterations_run == 30
+    assert np.array_equal(graph.residual_history, eager.residual_history)
+    assert torch.equal(graph.solution, eager.solution)
+
+
 def test_cg_generic_matches_fused(cuda):
     b, topo, geom, f = _cg_problem(3, 2, 2, 5)
     op = sb.GlobalOperator(geom, b, topo)
