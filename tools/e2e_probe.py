@@ -1,6 +1,7 @@
-"""Break down the host-buffer Ax path: chunk sizes, allocation, copies."""
+"""Host-buffer Ax path: per-step wall-time distribution and chunk sweep."""
 import ctypes
 import json
+import statistics
 import sys
 import time
 
@@ -18,51 +19,17 @@ b = sb.build_basis(n)
 u = sb.random_field(E, n, 1)
 geom = sb.GeomFactors(values=sb.random_field(6 * E, n, 2).reshape(E, 6, n, n, n))
 u_pin = u.cpu().pin_memory()
-out = torch.empty_like(u_pin).pin_memory()
-ud, wd = torch.empty_like(u), torch.empty_like(u)
-dx = np.ascontiguousarray(b.diff)
-lib = load()
-st = torch.cuda.current_stream()
-
-
-def run(chunk):
-    rc = lib.sem_ax_host(ctypes.c_void_p(u_pin.data_ptr()), dv.ptr(geom.values), dv.host_f64_ptr(dx),
-                         dv.host_f64_ptr(dx), ctypes.c_void_p(out.data_ptr()), E, n, dv.ptr(ud),
-                         dv.ptr(wd), chunk, ctypes.c_void_p(st.cuda_stream))
-    assert rc == 0, lib.sem_last_error()
-
-
 res = {}
-for chunk in [4096, 2048, 1024, 512, 256, 128, 64]:
-    for _ in range(3):
-        run(chunk)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(20):
-        run(chunk)
-        st.synchronize()
-    res[f"chunk{chunk}_ms"] = (time.perf_counter() - t0) / 20 * 1e3
-# side stream as the compute stream
-s2 = torch.cuda.Stream()
-with torch.cuda.stream(s2):
-    st = torch.cuda.current_stream()
-    for _ in range(3):
-        run(256)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(20):
-        run(256)
-        st.synchronize()
-    res["chunk256_sidestream_ms"] = (time.perf_counter() - t0) / 20 * 1e3
-# full API path
-for _ in range(3):
-    sb.apply_ax(u_pin, geom, b)
-t0 = time.perf_counter()
-for _ in range(20):
-    w = sb.apply_ax(u_pin, geom, b)
-res["api_ms"] = (time.perf_counter() - t0) / 20 * 1e3
-t0 = time.perf_counter()
-for _ in range(20):
-    o = torch.empty_like(u_pin, pin_memory=True)
-res["pinned_alloc_ms"] = (time.perf_counter() - t0) / 20 * 1e3
-print(json.dumps(res))
+for chunk_mb in (2, 4, 8, 16, 32):
+    K.HOST_CHUNK_BYTES = chunk_mb << 20
+    for _ in range(5):
+        w = sb.apply_ax(u_pin, geom, b)
+    ts = []
+    for _ in range(40):
+        t0 = time.perf_counter()
+        w = sb.apply_ax(u_pin, geom, b)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    ts.sort()
+    res[f"chunk{chunk_mb}MB"] = {"median_ms": statistics.median(ts), "min_ms": ts[0],
+                                 "p90_ms": ts[int(0.9 * len(ts))], "max_ms": ts[-1]}
+print(json.dumps(res, indent=1))
