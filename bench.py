@@ -38,6 +38,18 @@ METRIC = "Ax FP64 GFLOP/s at E=4096,p=9 (1/2/4/8 GPU) and % of B200 HBM roofline
 UNIT = "GFLOP/s"
 
 
+def max_over_ranks(value: float, dev) -> float:
+    """Max of a per-rank scalar (device tensor over NCCL, host tensor over gloo)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return value
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([value], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def ax_flops(E, n):
     return E * n ** 3 * (12 * n + 15)  # sembench/kernels.py:121-125
 
@@ -217,7 +229,10 @@ def run_ours(args, rank, world, local_rank):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            if dist.get_backend() == "nccl":
+                dist.barrier(device_ids=[local_rank])
+            else:
+                dist.barrier()
 
     for i in range(max(args.warmup, 3)):
         step(i)
@@ -245,9 +260,7 @@ def run_ours(args, rank, world, local_rank):
     ms_total = ev0.elapsed_time(ev1)
     ms_step = ms_total / args.steps
     if world > 1:
-        t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
+        ms_step = max_over_ranks(ms_step, dev)
     flops = ax_flops(E, n)
     value = world * flops / (ms_step * 1e-3) / 1e9
     peaks = measured_peaks(ROOT)
@@ -276,9 +289,7 @@ def run_ours(args, rank, world, local_rank):
     e2e_mean = t_all / e2e_steps
     e2e_p90 = sorted(per_step)[int(0.9 * (len(per_step) - 1))]
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s, dev)
     assert w_host.device.type == "cpu"
     e2e_val = world * flops / e2e_s / 1e9
 
@@ -408,7 +419,10 @@ def bench_cg_weak(sb, dev, world, rank, iters):
         ops = CudaSlabOps(part, geom_l.values, b, iters, dev)
         dist_cg_solve(ops, comm, f_l, 3)
         torch.cuda.synchronize(dev)
-        dist.barrier(device_ids=[dev.index])
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[dev.index])
+        else:
+            dist.barrier()
         ev0.record()
         res = dist_cg_solve(ops, comm, f_l, iters)
         ev1.record()
@@ -417,9 +431,7 @@ def bench_cg_weak(sb, dev, world, rank, iters):
         path = "z-slab partition, NCCL halo (2 ordered P2P steps) + rank-ordered all_gather"
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     per_it = ms / iters
     dofs_total = e_total * n ** 3
     model = perf.model_flops_per_iteration(dofs_total, n) / (per_it * 1e-3)
@@ -450,13 +462,20 @@ def main(argv=None):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: run a multi-rank job on ONE GPU (gloo; functional check of the
+    # N>1 code path only -- timings of such a run are meaningless)
+    if os.environ.get("SEM_BENCH_SHARE_GPU") == "1":
+        local_rank = 0
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("SEM_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         return run_ours(args, rank, world, local_rank)
     finally:
