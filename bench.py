@@ -428,7 +428,8 @@ def bench_cg_weak(sb, dev, world, rank, iters):
         ev1.record()
         torch.cuda.synchronize(dev)
         hist_last = float(res.residual_history[-1])
-        path = "z-slab partition, NCCL halo (2 ordered P2P steps) + rank-ordered all_gather"
+        path = (f"z-slab partition, {dist.get_backend()} halo (2 ordered P2P steps, interior Ax "
+                "overlapping the first) + rank-ordered all_gather")
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         ms = max_over_ranks(ms, dev)

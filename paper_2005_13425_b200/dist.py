@@ -137,9 +137,26 @@ class SlabComm:
 
     def exchange_up(self, top_partial, bottom_prefix) -> None:
         """Send this slab's top-face partial to rank+1; receive rank-1's."""
+        self.exchange_up_wait(self.exchange_up_start(top_partial, bottom_prefix))
+
+    def exchange_up_start(self, top_partial, bottom_prefix):
+        """Non-blocking form: returns a handle for exchange_up_wait().  Over NCCL
+        the transfer runs on the communicator's stream, so kernels enqueued on
+        the current stream before the wait overlap it."""
         p = self.part
-        self._xfer([(top_partial, p.upper)] if p.upper is not None else [],
-                   [(bottom_prefix, p.lower)] if p.lower is not None else [])
+        sends = [(top_partial, p.upper)] if p.upper is not None else []
+        recvs = [(bottom_prefix, p.lower)] if p.lower is not None else []
+        if self.stage:
+            self._xfer(sends, recvs)
+            return None
+        ops = [dist.P2POp(dist.isend, t, peer, self.group) for t, peer in sends]
+        ops += [dist.P2POp(dist.irecv, t, peer, self.group) for t, peer in recvs]
+        return dist.batch_isend_irecv(ops) if ops else None
+
+    @staticmethod
+    def exchange_up_wait(handle) -> None:
+        for req in handle or []:
+            req.wait()
 
     def exchange_down(self, bottom_totals, top_totals) -> None:
         """Send the bottom interface totals to rank-1; receive rank+1's."""
@@ -206,12 +223,22 @@ class CudaSlabOps:
     def p_update(self) -> None:
         """p = beta p + r is fused into the Ax launch (sem_cg_ax) below."""
 
-    def ax(self) -> None:
+    def ax_layers(self, l0: int, l1: int) -> None:
+        """p = beta p + r and w = A_local p on the slab's element layers [l0, l1)."""
         p = self.part
-        check(self.lib.sem_cg_ax(dv.ptr(self.p), dv.ptr(self.r), dv.ptr(self.g),
+        if l1 <= l0:
+            return
+        per = p.ex * p.ey
+        e0, ne = l0 * per, (l1 - l0) * per
+        off = lambda t, width: ctypes.c_void_p(t.data_ptr() + e0 * width * 8)  # noqa: E731
+        nnn = p.n ** 3
+        check(self.lib.sem_cg_ax(off(self.p, nnn), off(self.r, nnn), off(self.g, 6 * nnn),
                                  dv.host_f64_ptr(self.dx), dv.host_f64_ptr(self.dxt),
-                                 dv.ptr(self.w), p.num_elements, p.n, dv.ptr(self.state),
+                                 off(self.w, nnn), ne, p.n, dv.ptr(self.state),
                                  dv.ptr(self.history), self._s()), "dist cg ax")
+
+    def ax(self) -> None:
+        self.ax_layers(0, self.part.ez)
 
     def plane_top(self, field: torch.Tensor) -> torch.Tensor:
         p = self.part
@@ -259,12 +286,16 @@ class CudaSlabOps:
         return self.x, hist, iters, int(st.stop), float(st.pap), int(st.breakdown_it)
 
 
-def halo_exchange(ops, comm: SlabComm, field):
+def halo_exchange(ops, comm: SlabComm, field, overlap=None):
     """The two-step ordered halo of one assembled field.  Returns the
-    (bottom_totals, top_totals) planes this rank needs (None = no neighbour)."""
+    (bottom_totals, top_totals) planes this rank needs (None = no neighbour).
+    `overlap()` (optional) is enqueued while the first exchange is in flight."""
     part = comm.part
     top = ops.plane_top(field) if part.upper is not None else None
-    comm.exchange_up(top, ops.bottom_prefix if part.lower is not None else None)
+    handle = comm.exchange_up_start(top, ops.bottom_prefix if part.lower is not None else None)
+    if overlap is not None:
+        overlap()
+    comm.exchange_up_wait(handle)
     bot = ops.plane_bottom(field, ops.bottom_prefix) if part.lower is not None else None
     comm.exchange_down(bot, ops.top_totals if part.upper is not None else None)
     return bot, (ops.top_totals if part.upper is not None else None)
@@ -292,10 +323,16 @@ def dist_cg_solve(ops, comm: SlabComm, f_local, max_iterations: int, tolerance: 
     gathered = ops.scalar_buffer(world)
     ops.init(f_local, max_iterations, tolerance)
     ops.finish(0, comm.allgather(ops.local_sum(), gathered))
+    ez = part.ez
+    # the interface planes need only the bottom and top element layers: apply
+    # the operator there first and overlap the interior with the first exchange
+    edge = [(0, 1)] if ez == 1 else [(0, 1), (ez - 1, ez)]
     for _ in range(max_iterations):
         ops.p_update()
-        ops.ax()
-        bot, top = halo_exchange(ops, comm, ops.w)
+        for l0, l1 in edge:
+            ops.ax_layers(l0, l1)
+        bot, top = halo_exchange(ops, comm, ops.w,
+                                 overlap=lambda: ops.ax_layers(1, ez - 1) if ez > 2 else None)
         ops.assemble(bot, top)
         ops.finish(1, comm.allgather(ops.local_sum(), gathered))
         ops.update()

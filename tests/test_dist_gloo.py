@@ -106,8 +106,15 @@ class NumpySlabOps:
         beta = 0.0 if it == 1 else st["rtz"] / st["rtz_old"]
         O.scale_add(self.p, self.r, beta)
 
-    def ax(self):
-        self.w = O.ax_layered(self.p, self.g, self.dx, self.dxt)
+    def ax_layers(self, l0, l1):
+        if l1 <= l0:
+            return
+        if not hasattr(self, "w") or self.w is None or self.w.shape != self.p.shape:
+            self.w = np.zeros_like(self.p)
+        per = self.part.ex * self.part.ey
+        a, b = l0 * per, l1 * per
+        self.w[a:b] = O.ax_layered(np.ascontiguousarray(self.p[a:b]), self.g[a:b], self.dx,
+                                   self.dxt)
 
     def _plane(self, field, sel, prefix):
         acc = np.zeros(self.part.plane_size) if prefix is None else prefix.numpy().copy()
