@@ -67,10 +67,12 @@ int sem_ax_variant(const double *u, const double *g, const double *dx,
 int sem_ax_num_variants(int32_t n);
 
 /* Host-buffer form (the reference's call shape: u and w in host memory).
- * u_host / w_host should be page-locked for the copies to overlap; u_dev and
- * w_dev are E*n^3 device scratch vectors.  The element range is streamed in
- * chunks of `chunk_elements` (<= 0: one chunk): H2D of chunk c+1, Ax of chunk
- * c and D2H of chunk c-1 run concurrently on library-owned copy streams.
+ * If both u_host and w_host are page-locked (mapped), the kernel reads u and
+ * writes w across PCIe itself in one launch.  Otherwise u_dev and w_dev
+ * (E*n^3 device scratch vectors, always required) stage the data: the
+ * element range is streamed in chunks of `chunk_elements` (<= 0: one chunk),
+ * H2D of chunk c+1, Ax of chunk c and D2H of chunk c-1 running concurrently
+ * on library-owned copy streams.
  * Asynchronous: w_host is complete once `stream` has been synchronised. */
 int sem_ax_host(const double *u_host, const double *g, const double *dx,
                 const double *dxt, double *w_host, int64_t num_elements, int32_t n,

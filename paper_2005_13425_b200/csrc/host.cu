@@ -3,11 +3,15 @@
 //
 // A reference-style caller holds u and w in host memory.  Copying the whole
 // field in, computing, and copying it out serialises ~0.7 ms of H2D, 45 us
-// of compute and ~0.7 ms of D2H.  Here the element range is cut into chunks
-// and three streams run H2D of chunk c+1, Ax of chunk c and D2H of chunk c-1
-// concurrently (PCIe is full duplex), so the call costs ~max(H2D, D2H).
-// The chunk loop runs in C (no per-chunk host-language overhead); the two
-// copy streams and an event pool are created once per device and reused.
+// of compute and ~0.7 ms of D2H.  When both host buffers are page-locked
+// (mapped into the device address space) the Ax kernel itself loads u from
+// and stores w to host memory: one launch, the PCIe reads of later elements
+// overlap the writes of earlier ones, no copy-engine handoffs.  Pageable
+// buffers (or SEM_HOST_MODE=0) take the streamed path: the element range is
+// cut into chunks and three streams run H2D of chunk c+1, Ax of chunk c and
+// D2H of chunk c-1 concurrently (PCIe is full duplex).  The chunk loop runs
+// in C; the copy streams and an event pool are created once per device.
+#include <cstdlib>
 #include <mutex>
 
 #include "sem_common.cuh"
@@ -20,7 +24,14 @@ int ax_dispatch(const double* u, const double* g, const double* dx, double* w, i
 namespace {
 
 constexpr int kMaxDevices = 64;
-constexpr int kEventPool = 2 * 256 + 2;
+constexpr int kMaxChunks = 256;
+// Default transfer mode (tools/e2e_probe.py, B200 + PCIe Gen5, E=4096 p=9):
+// 0 = chunked copy engines both ways (0.97 ms), 1 = the kernel reads u and
+// writes w in mapped host memory itself (0.94 ms; 0.91 ms without the Python
+// wrapper), 2 = copy-engine u + mapped w (0.94 ms at 4 MB chunks), 3 = mapped
+// u + copy-engine w (1.17 ms).
+constexpr int kHostMode = 1;
+constexpr int kEventPool = 2 * kMaxChunks + 2;
 
 struct DevicePipes {
     bool ready = false;
@@ -55,6 +66,32 @@ int get_pipes(DevicePipes** out)
     return 0;
 }
 
+// Device address of a mapped page-locked host buffer, or nullptr (pageable).
+double* mapped(const double* host)
+{
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr) return nullptr;
+    return static_cast<double*>(at.devicePointer);
+}
+
+// Uniform chunk sizes (elements) for a streamed call; returns the count.
+// (A geometric ramp at both ends of the pipeline measured slower on B200 +
+// PCIe Gen5: every extra chunk costs more than the fill it saves.)
+int chunk_schedule(int64_t num_elements, int64_t base, int64_t* sizes)
+{
+    if (base <= 0 || base > num_elements) base = num_elements;
+    if ((num_elements + base - 1) / base > kMaxChunks)
+        base = (num_elements + kMaxChunks - 1) / kMaxChunks;
+    int k = 0;
+    for (int64_t e0 = 0; e0 < num_elements; e0 += base)
+        sizes[k++] = (e0 + base < num_elements) ? base : num_elements - e0;
+    return k;
+}
+
 }  // namespace
 }  // namespace sem
 
@@ -78,36 +115,51 @@ extern "C" int sem_ax_host(const double* u_host, const double* g, const double* 
     // shared, and stream ordering keeps back-to-back calls correct
     std::lock_guard<std::mutex> lock(g_enqueue_mu);
     const int64_t per = (int64_t)n * n * n;
-    int64_t chunk = chunk_elements > 0 ? chunk_elements : num_elements;
-    int64_t nchunks = (num_elements + chunk - 1) / chunk;
-    if (nchunks > 256) {  // bounded by the event pool
-        chunk = (num_elements + 255) / 256;
-        nchunks = (num_elements + chunk - 1) / chunk;
-    }
+    // Which side of the link each field crosses by copy engine and which by
+    // the kernel's own loads/stores of mapped page-locked memory (UVA).
+    // Pageable buffers have no device mapping and always use the copy engine.
+    int mode = kHostMode;
+    if (const char* env = getenv("SEM_HOST_MODE")) mode = atoi(env);  // tuning probe
+    double* u_map = mapped(u_host);
+    double* w_map = mapped(w_host);
+    const bool zc_in = (mode == 1 || mode == 3) && u_map;
+    const bool zc_out = (mode == 1 || mode == 2) && w_map;
+    if (zc_in && zc_out)  // one launch: PCIe reads and writes of all elements overlap
+        return ax_dispatch(u_map, g, dx, w_map, num_elements, n, 0, s);
+    int64_t sizes[kMaxChunks];
+    const int nchunks = chunk_schedule(num_elements, chunk_elements, sizes);
     cudaError_t err;
     // the copy streams start after everything already queued on `stream`
     err = cudaEventRecord(P->ev[0], s);
     if (err == cudaSuccess) err = cudaStreamWaitEvent(P->s_in, P->ev[0], 0);
     if (err == cudaSuccess) err = cudaStreamWaitEvent(P->s_out, P->ev[0], 0);
     if (err != cudaSuccess) return fail_cuda(err, "sem_ax_host: ordering");
-    for (int64_t c = 0; c < nchunks; ++c) {
-        const int64_t e0 = c * chunk;
-        const int64_t e1 = (e0 + chunk < num_elements) ? e0 + chunk : num_elements;
+    int64_t e0 = 0;
+    for (int c = 0; c < nchunks; ++c) {
+        const int64_t e1 = e0 + sizes[c];
         const int64_t a = e0 * per;
         const size_t bytes = (size_t)((e1 - e0) * per) * sizeof(double);
         cudaEvent_t ev_in = P->ev[2 + 2 * c], ev_k = P->ev[3 + 2 * c];
-        err = cudaMemcpyAsync(u_dev + a, u_host + a, bytes, cudaMemcpyHostToDevice, P->s_in);
-        if (err == cudaSuccess) err = cudaEventRecord(ev_in, P->s_in);
-        if (err == cudaSuccess) err = cudaStreamWaitEvent(s, ev_in, 0);
-        if (err != cudaSuccess) return fail_cuda(err, "sem_ax_host: H2D");
-        if (int rc = ax_dispatch(u_dev + a, g + e0 * 6 * per, dx, w_dev + a, e1 - e0, n, 0, s))
-            return rc;
-        err = cudaEventRecord(ev_k, s);
-        if (err == cudaSuccess) err = cudaStreamWaitEvent(P->s_out, ev_k, 0);
-        if (err == cudaSuccess)
-            err = cudaMemcpyAsync(w_host + a, w_dev + a, bytes, cudaMemcpyDeviceToHost, P->s_out);
-        if (err != cudaSuccess) return fail_cuda(err, "sem_ax_host: D2H");
+        const double* ku = zc_in ? u_map + a : u_dev + a;
+        double* kw = zc_out ? w_map + a : w_dev + a;
+        if (!zc_in) {
+            err = cudaMemcpyAsync(u_dev + a, u_host + a, bytes, cudaMemcpyHostToDevice, P->s_in);
+            if (err == cudaSuccess) err = cudaEventRecord(ev_in, P->s_in);
+            if (err == cudaSuccess) err = cudaStreamWaitEvent(s, ev_in, 0);
+            if (err != cudaSuccess) return fail_cuda(err, "sem_ax_host: H2D");
+        }
+        if (int rc = ax_dispatch(ku, g + e0 * 6 * per, dx, kw, e1 - e0, n, 0, s)) return rc;
+        if (!zc_out) {
+            err = cudaEventRecord(ev_k, s);
+            if (err == cudaSuccess) err = cudaStreamWaitEvent(P->s_out, ev_k, 0);
+            if (err == cudaSuccess)
+                err = cudaMemcpyAsync(w_host + a, w_dev + a, bytes, cudaMemcpyDeviceToHost,
+                                      P->s_out);
+            if (err != cudaSuccess) return fail_cuda(err, "sem_ax_host: D2H");
+        }
+        e0 = e1;
     }
+    if (zc_out) return 0;  // the kernels on `stream` wrote w_host themselves
     // the caller's stream completes only when the last D2H has landed
     err = cudaEventRecord(P->ev[1], P->s_out);
     if (err == cudaSuccess) err = cudaStreamWaitEvent(s, P->ev[1], 0);

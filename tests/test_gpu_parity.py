@@ -102,10 +102,14 @@ def test_ax_large_properties(cuda):
     assert O.rel_diff(au[idx].cpu().numpy(), ref) <= AX_TOL
 
 
+@pytest.mark.parametrize("mode", ["1", "0", "2", "3"])
 @pytest.mark.parametrize("kind", ["numpy", "pinned", "pageable"])
-def test_ax_host_streaming(cuda, kind):
-    """Host-buffer calls go through the chunked H2D/compute/D2H pipeline
-    (several chunks at E=1500, n=10); results match the device path exactly."""
+def test_ax_host_streaming(cuda, kind, mode, monkeypatch):
+    """Host-buffer calls: the mapped single-launch path (mode 1, default) and
+    the chunked copy-engine pipelines (several chunks at E=1500, n=10, with u
+    and/or w streamed by copy engines); results match the device path
+    exactly."""
+    monkeypatch.setenv("SEM_HOST_MODE", mode)
     E, n = 1500, 10
     b = sb.build_basis(n)
     u = sb.random_field(E, n, 9)
