@@ -16,6 +16,8 @@
  * /root/reference/pkg/src/sembench/):
  *
  *   sem_ax             kernels.py:413-468 apply_ax (LAYERED, :267-410)
+ *   sem_ax_reference   kernels.py:159-205 _ax_reference (REFERENCE variant)
+ *   sem_ax_scratch     kernels.py:213-259 _ax_scratch   (SCRATCH variant)
  *   sem_dssum_box      assembly.py:113-120 dssum  (bincount order, bit-exact)
  *   sem_mask_box       assembly.py:123-129 mask
  *   sem_apply_global   assembly.py:132-155 apply_global
@@ -77,6 +79,19 @@ int sem_ax_num_variants(int32_t n);
 int sem_ax_host(const double *u_host, const double *g, const double *dx,
                 const double *dxt, double *w_host, int64_t num_elements, int32_t n,
                 double *u_dev, double *w_dev, int64_t chunk_elements, sem_stream_t stream);
+
+/* The reference's other two storage strategies (kernels.py:1-45), bit-exact
+ * with sembench (same operation order, no FMA contraction).  REFERENCE: three
+ * passes through caller-provided full-size intermediates ur, us, ut
+ * ([E][n][n][n] device), which hold the metric-scaled gradients on return
+ * (kernels.py:159-205).  SCRATCH: element staged in shared memory, n <=
+ * SEM_SCRATCH_MAX_POINTS (kernels.py:213-259, :448-455). */
+#define SEM_SCRATCH_MAX_POINTS 10
+int sem_ax_reference(const double *u, const double *g, const double *dx,
+                     const double *dxt, double *ur, double *us, double *ut, double *w,
+                     int64_t num_elements, int32_t n, sem_stream_t stream);
+int sem_ax_scratch(const double *u, const double *g, const double *dx, double *w,
+                   int64_t num_elements, int32_t n, sem_stream_t stream);
 
 /* ------------------------------------------------- assembly (box mesh) -- */
 /* Element numbering e = ix + ex*(iy + ey*iz) and lattice ids of

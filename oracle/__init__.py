@@ -47,6 +47,10 @@ def lib():
         L.oracle_ax_layered.argtypes = [_dp, _dp, _dp, _dp, _dp, ctypes.c_int64,
                                         ctypes.c_int, ctypes.c_int]
         L.oracle_ax_layered.restype = ctypes.c_int
+        L.oracle_ax_reference.argtypes = [_dp] * 8 + [ctypes.c_int64, ctypes.c_int, ctypes.c_int]
+        L.oracle_ax_reference.restype = ctypes.c_int
+        L.oracle_ax_scratch.argtypes = [_dp] * 4 + [ctypes.c_int64, ctypes.c_int, ctypes.c_int]
+        L.oracle_ax_scratch.restype = ctypes.c_int
         L.oracle_dssum.argtypes = [_dp, _i64p, ctypes.c_int64, ctypes.c_int64, _dp]
         L.oracle_dssum.restype = ctypes.c_int
         L.oracle_mask.argtypes = [_dp, _dp, _dp, ctypes.c_int64]
@@ -176,6 +180,38 @@ def ax_layered(u: np.ndarray, g: np.ndarray, dx: np.ndarray, dxt: np.ndarray,
     rc = lib().oracle_ax_layered(_p(u), _p(g), _p(dx), _p(dxt), _p(w), E, n, nthreads)
     if rc != 0:
         raise RuntimeError(f"oracle_ax_layered failed ({rc})")
+    return w
+
+
+def ax_reference(u: np.ndarray, g: np.ndarray, dx: np.ndarray, dxt: np.ndarray,
+                 nthreads: int = 0):
+    """REFERENCE variant (sembench/kernels.py:159-205): returns (w, ur, us, ut),
+    the intermediates as the reference leaves them in its workspace."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    dx = np.ascontiguousarray(dx, dtype=np.float64)
+    dxt = np.ascontiguousarray(dxt, dtype=np.float64)
+    E, n = u.shape[0], u.shape[-1]
+    assert g.shape == (E, 6, n, n, n)
+    w, ur, us, ut = (np.empty_like(u) for _ in range(4))
+    rc = lib().oracle_ax_reference(_p(u), _p(g), _p(dx), _p(dxt), _p(ur), _p(us), _p(ut),
+                                   _p(w), E, n, nthreads)
+    if rc != 0:
+        raise RuntimeError(f"oracle_ax_reference failed ({rc})")
+    return w, ur, us, ut
+
+
+def ax_scratch(u: np.ndarray, g: np.ndarray, dx: np.ndarray, nthreads: int = 0) -> np.ndarray:
+    """SCRATCH variant (sembench/kernels.py:213-259)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    dx = np.ascontiguousarray(dx, dtype=np.float64)
+    E, n = u.shape[0], u.shape[-1]
+    assert g.shape == (E, 6, n, n, n)
+    w = np.empty_like(u)
+    rc = lib().oracle_ax_scratch(_p(u), _p(g), _p(dx), _p(w), E, n, nthreads)
+    if rc != 0:
+        raise RuntimeError(f"oracle_ax_scratch failed ({rc})")
     return w
 
 

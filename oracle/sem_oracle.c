@@ -14,6 +14,11 @@
  *                       at n = 10 the reference dispatches to :332-410 whose
  *                       sums start from the first product instead of 0.0 --
  *                       identical except for the sign of an all-zero sum.
+ *   oracle_ax_reference sembench/kernels.py:159-205 (REFERENCE: three full
+ *                       passes through E*n^3 intermediates ur/us/ut, which
+ *                       hold the metric-scaled gradients on return)
+ *   oracle_ax_scratch   sembench/kernels.py:213-259 (SCRATCH: element staged,
+ *                       phase 2 reads D transposed in place of diff_t)
  *   oracle_dssum        sembench/assembly.py:113-120 (np.bincount order:
  *                       ascending local index, accumulator starts at +0.0)
  *   oracle_wdot3        sembench/cg.py:77-92 (65536-point chunks, in order)
@@ -137,6 +142,120 @@ int oracle_ax_layered(const double *u, const double *g, const double *dx,
                                col_u, col_w, lay, lay + n * n, lay + 2 * n * n,
                                lay + 3 * n * n);
             free(buf);
+        }
+    }
+    return status;
+}
+
+/* REFERENCE variant: derivative pass -> geometric pass (in place) ->
+ * transpose pass, each over all elements.  Sums start at 0.0 and add the
+ * l-th product in ascending l; the transpose pass interleaves r, s, t terms
+ * per l (kernels.py:196-203). */
+int oracle_ax_reference(const double *u, const double *g, const double *dx,
+                        const double *dxt, double *ur, double *us, double *ut, double *w,
+                        int64_t num_elements, int n, int nthreads)
+{
+    if (n < 2 || n > 16 || num_elements < 0) return 1;
+    set_threads(nthreads);
+    const int64_t nnn = (int64_t)n * n * n;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < num_elements; ++e) {
+        const double *ue = u + e * nnn;
+        for (int k = 0; k < n; ++k)
+            for (int j = 0; j < n; ++j)
+                for (int i = 0; i < n; ++i) {
+                    double ar = 0.0, as = 0.0, at = 0.0;
+                    for (int l = 0; l < n; ++l) {
+                        ar += dx[i * n + l] * ue[(k * n + j) * n + l];
+                        as += dx[j * n + l] * ue[(k * n + l) * n + i];
+                        at += dx[k * n + l] * ue[(l * n + j) * n + i];
+                    }
+                    const int64_t q = e * nnn + (k * n + j) * n + i;
+                    ur[q] = ar;
+                    us[q] = as;
+                    ut[q] = at;
+                }
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < num_elements; ++e)
+        for (int64_t p = 0; p < nnn; ++p) {
+            const int64_t q = e * nnn + p;
+            const double *ge = g + e * 6 * nnn + p;
+            const double wr = ur[q], ws = us[q], wt = ut[q];
+            const double g1 = ge[0], g2 = ge[nnn], g3 = ge[2 * nnn];
+            const double g4 = ge[3 * nnn], g5 = ge[4 * nnn], g6 = ge[5 * nnn];
+            ur[q] = g1 * wr + g2 * ws + g3 * wt;
+            us[q] = g2 * wr + g4 * ws + g5 * wt;
+            ut[q] = g3 * wr + g5 * ws + g6 * wt;
+        }
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < num_elements; ++e) {
+        const double *re = ur + e * nnn, *se = us + e * nnn, *te = ut + e * nnn;
+        for (int k = 0; k < n; ++k)
+            for (int j = 0; j < n; ++j)
+                for (int i = 0; i < n; ++i) {
+                    double acc = 0.0;
+                    for (int l = 0; l < n; ++l) {
+                        acc += dxt[i * n + l] * re[(k * n + j) * n + l];
+                        acc += dxt[j * n + l] * se[(k * n + l) * n + i];
+                        acc += dxt[k * n + l] * te[(l * n + j) * n + i];
+                    }
+                    w[e * nnn + (k * n + j) * n + i] = acc;
+                }
+    }
+    return 0;
+}
+
+/* SCRATCH variant: per element, phase 1 with the metric applied per point,
+ * then phase 2 with D read transposed (sd[l][i] for diff_t[i][l]). */
+int oracle_ax_scratch(const double *u, const double *g, const double *dx, double *w,
+                      int64_t num_elements, int n, int nthreads)
+{
+    if (n < 2 || n > 16 || num_elements < 0) return 1;
+    set_threads(nthreads);
+    const int64_t nnn = (int64_t)n * n * n;
+    int status = 0;
+#pragma omp parallel
+    {
+        double *sr = (double *)malloc(sizeof(double) * 3 * (size_t)nnn);
+        if (!sr) {
+#pragma omp atomic write
+            status = 2;
+        } else {
+            double *ss = sr + nnn, *st = sr + 2 * nnn;
+#pragma omp for schedule(static)
+            for (int64_t e = 0; e < num_elements; ++e) {
+                const double *ue = u + e * nnn, *ge = g + e * 6 * nnn;
+                for (int k = 0; k < n; ++k)
+                    for (int j = 0; j < n; ++j)
+                        for (int i = 0; i < n; ++i) {
+                            double wr = 0.0, ws = 0.0, wt = 0.0;
+                            for (int l = 0; l < n; ++l) {
+                                wr += dx[i * n + l] * ue[(k * n + j) * n + l];
+                                ws += dx[j * n + l] * ue[(k * n + l) * n + i];
+                                wt += dx[k * n + l] * ue[(l * n + j) * n + i];
+                            }
+                            const int p = (k * n + j) * n + i;
+                            const double g1 = ge[p], g2 = ge[nnn + p], g3 = ge[2 * nnn + p];
+                            const double g4 = ge[3 * nnn + p], g5 = ge[4 * nnn + p];
+                            const double g6 = ge[5 * nnn + p];
+                            sr[p] = g1 * wr + g2 * ws + g3 * wt;
+                            ss[p] = g2 * wr + g4 * ws + g5 * wt;
+                            st[p] = g3 * wr + g5 * ws + g6 * wt;
+                        }
+                for (int k = 0; k < n; ++k)
+                    for (int j = 0; j < n; ++j)
+                        for (int i = 0; i < n; ++i) {
+                            double acc = 0.0;
+                            for (int l = 0; l < n; ++l) {
+                                acc += dx[l * n + i] * sr[(k * n + j) * n + l];
+                                acc += dx[l * n + j] * ss[(k * n + l) * n + i];
+                                acc += dx[l * n + k] * st[(l * n + j) * n + i];
+                            }
+                            w[e * nnn + (k * n + j) * n + i] = acc;
+                        }
+            }
+            free(sr);
         }
     }
     return status;

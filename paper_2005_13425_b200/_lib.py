@@ -53,6 +53,8 @@ SIGNATURES = {
     "sem_max_points": (ctypes.c_int, []),
     "sem_ax": (ctypes.c_int, [_vp, _vp, _dp, _dp, _vp, _i64, _i32, _vp]),
     "sem_ax_variant": (ctypes.c_int, [_vp, _vp, _dp, _dp, _vp, _i64, _i32, _i32, _vp]),
+    "sem_ax_reference": (ctypes.c_int, [_vp, _vp, _dp, _dp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
+    "sem_ax_scratch": (ctypes.c_int, [_vp, _vp, _dp, _vp, _i64, _i32, _vp]),
     "sem_ax_num_variants": (ctypes.c_int, [_i32]),
     "sem_ax_host": (ctypes.c_int, [_vp, _vp, _dp, _dp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
     "sem_dssum_box": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),

@@ -7,13 +7,18 @@ be loaded by ctypes from any host language; see include/sem.h.
 from __future__ import annotations
 
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsem.so")
-SOURCES = ["common.cu", "ax.cu", "assembly.cu", "cg.cu", "fields.cu", "host.cu", "slab.cu"]
+# ax_inst.cu is compiled once per n group (-DSEM_AX_GROUP=k) so the unrolled
+# per-n Ax instantiations build in parallel.
+AX_GROUPS = 8
+SOURCES = ["common.cu", "ax.cu", "ax_variants.cu", "assembly.cu", "cg.cu", "fields.cu", "host.cu", "slab.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -39,14 +44,33 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit concurrently (one nvcc per .cu), then
+    link the shared library."""
     if not force and not _stale():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    objdir = tempfile.mkdtemp(prefix="libsem_obj_")
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
     if verbose:
-        cmd += ["-Xptxas", "-v"]
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        compile_flags += ["-Xptxas", "-v"]
+    units = [(src, src.replace(".cu", ".o"), []) for src in SOURCES]
+    units += [("ax_inst.cu", f"ax_inst{k}.o", [f"-DSEM_AX_GROUP={k}"]) for k in range(AX_GROUPS)]
+    units.sort(key=lambda u: u[0] != "ax_inst.cu")  # longest jobs first
+    procs, objs = [], []
+    for src, objname, extra in units:
+        obj = os.path.join(objdir, objname)
+        objs.append(obj)
+        cmd = [nvcc(), *compile_flags, *extra, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((src, subprocess.Popen(cmd)))
+    failed = [src for src, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc ({', '.join(failed)})")
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+            "-o", OUT + ".tmp", *objs]
+    subprocess.run(link, check=True)
     os.replace(OUT + ".tmp", OUT)
+    shutil.rmtree(objdir, ignore_errors=True)
     return OUT
 
 

@@ -1,450 +1,36 @@
-// Local Poisson operator Ax on B200 (sm_100a), FP64.
-//
-// Algorithm: the LAYERED variant of sembench/kernels.py:267-410 (paper
-// §IV-C): a 2-D layer of threads walks the k layers of an element in lock
-// step; each thread keeps its u column and its w accumulator column in
-// registers, the r/s contractions of a layer read the layer (and its
-// phase-1 results) from shared memory, and the t contraction is a register
-// GEMV whose D entries are compile-time constant-bank operands.
-//
-// B200-specific layout decisions:
-//  * a thread owns an i-PAIR (i0, i0+1) of one (j) row, so every u / g / w
-//    global access is a coalesced 128-bit vector (ld.global.nc.v2.f64) and
-//    every shared-memory read of the layer is an LDS.128; odd n pads the
-//    shared layer to an even row stride with a zero phantom column.
-//  * D and D^T live in shared memory for the lane-varying (r, s) directions
-//    and in kernel-parameter constant space for the warp-uniform (t)
-//    direction -- so the t-direction costs no shared-memory traffic.
-//  * several elements ("slots") per CTA, double-buffered layer arrays so a
-//    layer needs two CTA barriers, and the next layer's six metric vectors
-//    are prefetched into registers while the current one computes.
-//
-// Arithmetic differs from the reference only by FMA contraction and
-// association (tolerance 1e-12 max-norm relative, sembench/verify.py:37-42).
-#include <math.h>
-#include <stdlib.h>
-
+// Local Poisson operator Ax on B200 (sm_100a): the C-ABI entry points and the
+// runtime-n dispatch.  The kernels are in ax_pencil.cuh / ax_impl.cuh and are
+// instantiated per n in ax_inst.cu.
 #include "sem_common.cuh"
-#include "ax_pencil.cuh"
 #include "box.cuh"
 
 namespace sem {
 
-template <int N>
-struct DParam {
-    double d[N * N];  // D[i][l] row-major (basis.diff)
-};
-
-__device__ __forceinline__ double2 ldg2(const double* p)
-{
-    double2 v;
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ double ldg1(const double* p)
-{
-    double v;
-    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ void stg2(double* p, double2 v)
-{
-    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
-}
-
-// Compile-time configuration per n.
-template <int N>
-struct AxCfg {
-    static constexpr int NE = (N + 1) & ~1;        // padded row length (even)
-    static constexpr int NP = NE / 2;              // i-pairs per row
-    static constexpr int TPE = NP * N;             // threads per element
-    static constexpr int NN = N * N;
-    static constexpr int NNN = N * N * N;
-    static constexpr int LAYER = NE * N;           // padded layer size (doubles)
-    // elements per CTA: aim at ~256-448 threads
-    static constexpr int SLOTS = (TPE >= 256) ? 1 : ((448 / TPE) < 1 ? 1 : (448 / TPE));
-    static constexpr int THREADS = ((SLOTS * TPE + 31) / 32) * 32;
-    static constexpr bool VEC = (N % 2) == 0;      // 16-B aligned global pairs
-};
-
-template <int N, int SLOTS>
-struct AxSmem {
-    static constexpr int NE = AxCfg<N>::NE;
-    static constexpr int LAYER = AxCfg<N>::LAYER;
-    alignas(16) double d[N * NE];    // d[i*NE + l]  = D[i][l]   (pad l>=N with 0)
-    alignas(16) double dt[NE * NE];  // dt[l*NE + i] = D[i][l]   (pad i>=N with 0)
-    alignas(16) double u[2][SLOTS][LAYER];
-    alignas(16) double r[2][SLOTS][LAYER];
-    alignas(16) double s[2][SLOTS][LAYER];
-};
-
-template <int N, int SLOTS, int THREADS>
-__global__ void __launch_bounds__(THREADS)
-ax_layered_kernel(const double* __restrict__ u, const double* __restrict__ g,
-                  double* __restrict__ w, int64_t num_elements, const DParam<N> D)
-{
-    using C = AxCfg<N>;
-    constexpr int NE = C::NE, NP = C::NP, TPE = C::TPE, NN = C::NN, NNN = C::NNN;
-    constexpr bool VEC = C::VEC;
-    __shared__ AxSmem<N, SLOTS> sm;
-
-    const int tid = threadIdx.x;
-    // D tables (padded with zeros so phantom rows/columns contribute 0)
-    for (int t = tid; t < N * NE; t += THREADS) {
-        const int i = t / NE, l = t % NE;
-        sm.d[t] = (l < N) ? D.d[i * N + l] : 0.0;
-    }
-    for (int t = tid; t < NE * NE; t += THREADS) {
-        const int l = t / NE, i = t % NE;
-        sm.dt[t] = (i < N && l < N) ? D.d[i * N + l] : 0.0;
-    }
-
-    const int slot = tid / TPE;
-    const int rem = tid - slot * TPE;
-    const int j = rem / NP;
-    const int i0 = 2 * (rem - j * NP);
-    const int64_t e = (int64_t)blockIdx.x * SLOTS + slot;
-    const bool active = (slot < SLOTS) && (e < num_elements);
-    const bool second = (i0 + 1) < N;  // false only for the phantom of odd n
-    const int sl = active ? slot : 0;
-
-    const double* ue = u + (active ? e : 0) * NNN + j * N + i0;
-    const double* ge = g + (active ? e : 0) * (6 * NNN) + j * N + i0;
-
-    // u column of the pair, all layers (coalesced 128-bit loads)
-    double2 uc[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        if (!active) {
-            uc[k] = make_double2(0.0, 0.0);
-        } else if (VEC) {
-            uc[k] = ldg2(ue + k * NN);
-        } else {
-            uc[k].x = ldg1(ue + k * NN);
-            uc[k].y = second ? ldg1(ue + k * NN + 1) : 0.0;
-        }
-    }
-    double2 acc[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) acc[k] = make_double2(0.0, 0.0);
-
-    auto load_g = [&](double2 (&gv)[6], int k) {
-#pragma unroll
-        for (int m = 0; m < 6; ++m) {
-            const double* p = ge + m * NNN + k * NN;
-            if (!active) {
-                gv[m] = make_double2(0.0, 0.0);
-            } else if (VEC) {
-                gv[m] = ldg2(p);
-            } else {
-                gv[m].x = ldg1(p);
-                gv[m].y = second ? ldg1(p + 1) : 0.0;
-            }
-        }
-    };
-    double2 gn[6];
-    load_g(gn, 0);
-    __syncthreads();
-
-    const double2* d2 = reinterpret_cast<const double2*>(sm.d);
-    const double2* dt2 = reinterpret_cast<const double2*>(sm.dt);
-
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        const int b = k & 1;
-        double* su = sm.u[b][sl];
-        double* sr = sm.r[b][sl];
-        double* ss = sm.s[b][sl];
-        if (active) *reinterpret_cast<double2*>(su + j * NE + i0) = uc[k];
-        double2 gc[6];
-#pragma unroll
-        for (int m = 0; m < 6; ++m) gc[m] = gn[m];
-        if (k + 1 < N) load_g(gn, k + 1);
-        __syncthreads();
-
-        // ---- phase 1: directional derivatives at layer k ----
-        const double2* su2 = reinterpret_cast<const double2*>(su);
-        double wr0 = 0.0, wr1 = 0.0, ws0 = 0.0, ws1 = 0.0, wt0 = 0.0, wt1 = 0.0;
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            const double2 ur = su2[(j * NE) / 2 + q];                 // U[j][2q..2q+1]
-            const double2 da = dt2[((2 * q) * NE + i0) / 2];          // D[i0..i0+1][2q]
-            const double2 dj = d2[(j * NE) / 2 + q];                  // D[j][2q..2q+1]
-            const double2 ua = su2[((2 * q) * NE + i0) / 2];          // U[2q][i0..i0+1]
-            wr0 = fma(da.x, ur.x, wr0);
-            wr1 = fma(da.y, ur.x, wr1);
-            ws0 = fma(dj.x, ua.x, ws0);
-            ws1 = fma(dj.x, ua.y, ws1);
-            if (2 * q + 1 < N) {
-                const double2 db = dt2[((2 * q + 1) * NE + i0) / 2];  // D[i0..][2q+1]
-                const double2 ub = su2[((2 * q + 1) * NE + i0) / 2];  // U[2q+1][i0..]
-                wr0 = fma(db.x, ur.y, wr0);
-                wr1 = fma(db.y, ur.y, wr1);
-                ws0 = fma(dj.y, ub.x, ws0);
-                ws1 = fma(dj.y, ub.y, ws1);
-            }
-        }
-#pragma unroll
-        for (int l = 0; l < N; ++l) {
-            const double dkl = D.d[k * N + l];  // warp-uniform: constant bank
-            wt0 = fma(dkl, uc[l].x, wt0);
-            wt1 = fma(dkl, uc[l].y, wt1);
-        }
-        // metric: (ur,us,ut) = G (wr,ws,wt), G = (g1 g2 g3; g2 g4 g5; g3 g5 g6)
-        const double r0 = fma(gc[2].x, wt0, fma(gc[1].x, ws0, gc[0].x * wr0));
-        const double r1 = fma(gc[2].y, wt1, fma(gc[1].y, ws1, gc[0].y * wr1));
-        const double s0 = fma(gc[4].x, wt0, fma(gc[3].x, ws0, gc[1].x * wr0));
-        const double s1 = fma(gc[4].y, wt1, fma(gc[3].y, ws1, gc[1].y * wr1));
-        const double t0 = fma(gc[5].x, wt0, fma(gc[4].x, ws0, gc[2].x * wr0));
-        const double t1 = fma(gc[5].y, wt1, fma(gc[4].y, ws1, gc[2].y * wr1));
-        if (active) {
-            *reinterpret_cast<double2*>(sr + j * NE + i0) = make_double2(r0, r1);
-            *reinterpret_cast<double2*>(ss + j * NE + i0) = make_double2(s0, s1);
-        }
-        __syncthreads();
-
-        // ---- phase 2: transposed contractions ----
-        const double2* sr2 = reinterpret_cast<const double2*>(sr);
-        const double2* ss2 = reinterpret_cast<const double2*>(ss);
-        double ar0 = 0.0, ar1 = 0.0, as0 = 0.0, as1 = 0.0;
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            const double2 rr = sr2[(j * NE) / 2 + q];                 // ur[j][2q..]
-            const double2 da = d2[((2 * q) * NE + i0) / 2];           // D[2q][i0..i0+1]
-            const double2 dj = dt2[(j * NE) / 2 + q];                 // D[2q..2q+1][j]
-            const double2 sa = ss2[((2 * q) * NE + i0) / 2];          // us[2q][i0..]
-            ar0 = fma(da.x, rr.x, ar0);
-            ar1 = fma(da.y, rr.x, ar1);
-            as0 = fma(dj.x, sa.x, as0);
-            as1 = fma(dj.x, sa.y, as1);
-            if (2 * q + 1 < N) {
-                const double2 db = d2[((2 * q + 1) * NE + i0) / 2];   // D[2q+1][i0..]
-                const double2 sb = ss2[((2 * q + 1) * NE + i0) / 2];
-                ar0 = fma(db.x, rr.y, ar0);
-                ar1 = fma(db.y, rr.y, ar1);
-                as0 = fma(dj.y, sb.x, as0);
-                as1 = fma(dj.y, sb.y, as1);
-            }
-        }
-        acc[k].x += ar0 + as0;
-        acc[k].y += ar1 + as1;
-#pragma unroll
-        for (int kk = 0; kk < N; ++kk) {
-            const double dkk = D.d[k * N + kk];  // D^T[kk][k]
-            acc[kk].x = fma(dkk, t0, acc[kk].x);
-            acc[kk].y = fma(dkk, t1, acc[kk].y);
-        }
-    }
-
-    if (active) {
-        double* we = w + e * NNN + j * N + i0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            if (VEC) {
-                stg2(we + k * NN, acc[k]);
-            } else {
-                we[k * NN] = acc[k].x;
-                if (second) we[k * NN + 1] = acc[k].y;
-            }
-        }
-    }
-}
-
-template <int N>
-static int launch_ax(const double* u, const double* g, const double* dx, double* w,
-                     int64_t E, cudaStream_t stream)
-{
-    using C = AxCfg<N>;
-    DParam<N> D;
-    for (int t = 0; t < N * N; ++t) D.d[t] = dx[t];
-    if (E == 0) return 0;
-    const int64_t blocks = (E + C::SLOTS - 1) / C::SLOTS;
-    if (blocks > 0x7fffffffLL) {
-        set_error("sem_ax: too many elements (%lld)", (long long)E);
-        return SEM_E_INVALID;
-    }
-    ax_layered_kernel<N, C::SLOTS, C::THREADS>
-        <<<(unsigned)blocks, C::THREADS, 0, stream>>>(u, g, w, E, D);
-    SEM_CHECK_LAUNCH("sem_ax launch");
-    return 0;
-}
-
-constexpr int kAxCarveout = -1;
-
-// Kernel-parameter D tables (one copy per stage) and their even-odd forms.
-// Returns whether D is centro-antisymmetric to 1e-13 relative, i.e. whether
-// the folded contraction is usable (it is for every GLL basis).
-template <int N>
-static bool fill_dparam(DParamP<N>& P, const double* dx)
-{
-    constexpr int H = N / 2, c = (N - 1) / 2;
-    double dev = 0.0, scale = 0.0;
-    for (int i = 0; i < N; ++i)
-        for (int l = 0; l < N; ++l) {
-            const double v = dx[i * N + l];
-            scale = fabs(v) > scale ? fabs(v) : scale;
-            const double d = fabs(dx[(N - 1 - i) * N + (N - 1 - l)] + v);
-            dev = d > dev ? d : dev;
-        }
-    for (int st = 0; st < 6; ++st) {
-        for (int t = 0; t < N * N; ++t) P.d[st][t] = dx[t];
-        const bool trans = (st == kStS4 || st == kStS5 || st == kStS6);
-        auto M = [&](int i, int l) { return trans ? dx[l * N + i] : dx[i * N + l]; };
-        for (int i = 0; i < H; ++i)
-            for (int l = 0; l < H; ++l) {
-                P.a[st][i * H + l] = 0.5 * (M(i, l) + M(i, N - 1 - l));
-                P.b[st][i * H + l] = 0.5 * (M(i, l) - M(i, N - 1 - l));
-            }
-        if (N % 2 == 1) {
-            for (int i = 0; i < H; ++i) P.mc[st][i] = M(i, c);
-            for (int l = 0; l < H; ++l) P.mr[st][l] = 0.5 * (M(c, l) - M(c, N - 1 - l));
-        }
-    }
-    return dev <= 1e-13 * scale;
-}
-
-template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
-          bool FOLD = false, bool CGP = false>
-static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
-                         int64_t E, cudaStream_t stream, CgpArgs cgp = CgpArgs{})
-{
-    using C = PencilCfg<N>;
-    constexpr int THREADS = ((SLOTS * C::NN + 31) / 32) * 32;
-    constexpr size_t SMEM = sizeof(double) * ((size_t)SLOTS * C::SLOT_DOUBLES +
-                                              (GMODE ? (size_t)SLOTS * 6 * C::NNN + 6 : 0));
-    static_assert(SMEM * MINB <= 227 * 1024, "pencil kernel shared memory");
-    DParamP<N> D;
-    const bool antisym = fill_dparam<N>(D, dx);
-    if constexpr (FOLD) {
-        if (!antisym)  // the even-odd form needs a centro-antisymmetric D
-            return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, false, CGP>(
-                u, g, dx, w, E, stream, cgp);
-    }
-    if (E == 0) return 0;
-    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGP>;
-    static bool configured = false;  // per template instance
-    if (!configured) {
-        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)SMEM);
-        if (err != cudaSuccess) return fail_cuda(err, "sem_ax: cudaFuncSetAttribute");
-        // smem/L1 split: the streaming u/g loads need L1 capacity for their
-        // in-flight lines, so the carveout is a tuning knob (measured in
-        // profiles/; SEM_AX_CARVEOUT overrides, -1 = driver default)
-        int carve = kAxCarveout;
-        if (const char* env = getenv("SEM_AX_CARVEOUT")) carve = atoi(env);
-        if (carve >= 0) {
-            err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-            if (err != cudaSuccess) return fail_cuda(err, "sem_ax: carveout");
-        }
-        configured = true;
-    }
-    const int64_t nbatches = (E + SLOTS - 1) / SLOTS;
-    const int64_t resident = (int64_t)sm_count() * MINB;
-    const int64_t grid = PERSIST ? (nbatches < resident ? nbatches : resident) : nbatches;
-    // prefetch distance: the batch that replaces this one on its SM
-    const int64_t pf = (nbatches > resident) ? resident * SLOTS : 0;
-    kern<<<(unsigned)grid, THREADS, SMEM, stream>>>(u, g, w, E, D, pf, cgp);
-    SEM_CHECK_LAUNCH("sem_ax (pencil) launch");
-    return 0;
-}
-
-template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
-          bool FOLD = false, bool CGP = false>
-static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
-                      cudaStream_t stream, CgpArgs cgp = CgpArgs{})
-{
-    if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 && (GMODE != 2 || N % 2 == 0) &&
-                  sizeof(double) * ((size_t)SLOTS * PencilCfg<N>::SLOT_DOUBLES +
-                                    (GMODE ? (size_t)SLOTS * 6 * N * N * N + 6 : 0)) * MINB <= 227 * 1024)
-        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGP>(u, g, dx, w, E,
-                                                                               stream, cgp);
-    else
-        return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, CGP>(
-            u, g, dx, w, E, stream, cgp);
-}
-
-// variant 0: the tuned default for this n (kDefaultVariant);
-// 1: per-point layered kernel (first B200 version, kept for ablation);
-// 2..19: pencil tuning points <elements per CTA, CTAs per SM, metric
-// prefetch depth, persistent, L2 bulk prefetch>.
-// Default tuning point per n (tools/ax_sweep.py on B200, E=4096; see
-// profiles/r01_ax_sweep.txt, CUDA-graph timed): index = n, value = variant id.
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 37, 34, 34, 35, 5, 8, 7, 17, 3};
-
-template <int N>
-static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
-                int variant, cudaStream_t stream)
-{
-    constexpr int S = PencilCfg<N>::SLOTS;
-    if (variant == 0) variant = kDefaultVariant[N];
-    switch (variant) {
-        case 19: return try_pencil<N, S, 1, false>(u, g, dx, w, E, stream);
-        case 20: return try_pencil<N, 1, 4, false, 3>(u, g, dx, w, E, stream);
-        case 21: return try_pencil<N, 1, 4, false, 4>(u, g, dx, w, E, stream);
-        case 22: return try_pencil<N, 1, 4, false, 5>(u, g, dx, w, E, stream);
-        case 23: return try_pencil<N, 1, 5, false, 2>(u, g, dx, w, E, stream);
-        case 24: return try_pencil<N, 1, 3, false, 5>(u, g, dx, w, E, stream);
-        case 25: return try_pencil<N, 1, 3, false, 1, false, 1>(u, g, dx, w, E, stream);
-        case 26: return try_pencil<N, 1, 2, false, 1, false, 1>(u, g, dx, w, E, stream);
-        case 27: return try_pencil<N, 1, 3, false, 1, false, 2>(u, g, dx, w, E, stream);
-        case 28: return try_pencil<N, 1, 4, false, 1, false, 1>(u, g, dx, w, E, stream);
-        case 29: return try_pencil<N, 1, 4, false, 1, false, 2>(u, g, dx, w, E, stream);
-        case 30: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 1>(u, g, dx, w, E, stream);
-        case 31: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream);
-        case 32: return try_pencil<N, (S + 2) / 3, 3, false, 1, false, 2>(u, g, dx, w, E, stream);
-        case 33: return try_pencil<N, 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream);
-        // even-odd folded contractions (centro-antisymmetric D only)
-        case 34: return try_pencil<N, 1, 3, false, 1, false, 1, true>(u, g, dx, w, E, stream);
-        case 35: return try_pencil<N, 1, 2, false, 1, false, 1, true>(u, g, dx, w, E, stream);
-        case 36: return try_pencil<N, 1, 5, false, 3, false, 0, true>(u, g, dx, w, E, stream);
-        case 37: return try_pencil<N, 1, 4, false, 1, false, 1, true>(u, g, dx, w, E, stream);
-        case 38: return try_pencil<N, 1, 3, false, 1, false, 2, true>(u, g, dx, w, E, stream);
-        case 39: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 1, true>(u, g, dx, w, E, stream);
-        case 1: return launch_ax<N>(u, g, dx, w, E, stream);
-        case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
-        case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
-        case 4: return try_pencil<N, (S + 1) / 2, 2, false, 2>(u, g, dx, w, E, stream);
-        case 5: return try_pencil<N, (S + 1) / 2, 2, false, 3>(u, g, dx, w, E, stream);
-        case 6: return try_pencil<N, (S + 2) / 3, 3, false>(u, g, dx, w, E, stream);
-        case 7: return try_pencil<N, (S + 2) / 3, 3, false, 2>(u, g, dx, w, E, stream);
-        case 8: return try_pencil<N, (S + 2) / 3, 3, false, 3>(u, g, dx, w, E, stream);
-        case 9: return try_pencil<N, 1, 6, false, 2>(u, g, dx, w, E, stream);
-        case 10: return try_pencil<N, (S + 2) / 3, 3, false, 1, true>(u, g, dx, w, E, stream);
-        case 11: return try_pencil<N, S + 1, 1, false, 2>(u, g, dx, w, E, stream);
-        case 12: return try_pencil<N, 1, 7, false, 1>(u, g, dx, w, E, stream);
-        case 13: return try_pencil<N, 1, 7, false, 2>(u, g, dx, w, E, stream);
-        case 14: return try_pencil<N, 1, 7, false, 3>(u, g, dx, w, E, stream);
-        case 15: return try_pencil<N, 1, 5, false, 3>(u, g, dx, w, E, stream);
-        case 16: return try_pencil<N, 1, 6, false, 3>(u, g, dx, w, E, stream);
-        case 17: return try_pencil<N, (S + 1) / 2, 2, false, 4>(u, g, dx, w, E, stream);
-        default:
-            set_error("sem_ax: unknown variant %d", variant);
-            return SEM_E_INVALID;
-    }
-}
-
-// CG iteration head fused with Ax (p = beta p + r; w = A_local p): the tuned
-// configuration of each n with the metric staged by TMA and u through
-// registers (the p update happens while the column is loaded).
-template <int N>
-static int ax_cg_n(double* p, const double* r, const double* g, const double* dx, double* w,
-                   int64_t E, sem_cg_state* st, double* hist, cudaStream_t s)
-{
-    const CgpArgs a{p, r, st, hist};
-    if constexpr (N >= 5 && N <= 11)
-        return try_pencil<N, 1, 3, false, 1, false, 1, true, true>(p, g, dx, w, E, s, a);
-    else if constexpr (N == 4)
-        return try_pencil<N, 1, 2, false, 1, false, 1, false, true>(p, g, dx, w, E, s, a);
-    else
-        return try_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, true>(p, g, dx, w,
-                                                                                    E, s, a);
-}
+#define SEM_AX_DECLARE(NV)                                                                   \
+    int ax_entry_##NV(const double* u, const double* g, const double* dx, double* w,          \
+                      int64_t E, int variant, cudaStream_t s);                                \
+    int ax_cg_entry_##NV(double* p, const double* r, const double* g, const double* dx,       \
+                         double* w, int64_t E, sem_cg_state* st, double* hist, cudaStream_t s);
+SEM_AX_DECLARE(2) SEM_AX_DECLARE(3) SEM_AX_DECLARE(4) SEM_AX_DECLARE(5) SEM_AX_DECLARE(6)
+SEM_AX_DECLARE(7) SEM_AX_DECLARE(8) SEM_AX_DECLARE(9) SEM_AX_DECLARE(10) SEM_AX_DECLARE(11)
+SEM_AX_DECLARE(12) SEM_AX_DECLARE(13) SEM_AX_DECLARE(14) SEM_AX_DECLARE(15) SEM_AX_DECLARE(16)
+#undef SEM_AX_DECLARE
 
 int ax_cg_dispatch(double* p, const double* r, const double* g, const double* dx, double* w,
                    int64_t E, int n, sem_cg_state* st, double* hist, cudaStream_t stream)
 {
     if (E == 0) return 0;
-    SEM_SWITCH_N(n, return ax_cg_n<NV>(p, r, g, dx, w, E, st, hist, stream));
+    switch (n) {
+#define SEM_AXCG_CASE(NV) \
+    case NV: return ax_cg_entry_##NV(p, r, g, dx, w, E, st, hist, stream);
+        SEM_AXCG_CASE(2) SEM_AXCG_CASE(3) SEM_AXCG_CASE(4) SEM_AXCG_CASE(5) SEM_AXCG_CASE(6)
+        SEM_AXCG_CASE(7) SEM_AXCG_CASE(8) SEM_AXCG_CASE(9) SEM_AXCG_CASE(10) SEM_AXCG_CASE(11)
+        SEM_AXCG_CASE(12) SEM_AXCG_CASE(13) SEM_AXCG_CASE(14) SEM_AXCG_CASE(15) SEM_AXCG_CASE(16)
+#undef SEM_AXCG_CASE
+        default:
+            set_error("sem_cg_ax: n=%d outside the supported range [2, 16]", n);
+            return SEM_E_INVALID;
+    }
 }
 
 int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
@@ -452,7 +38,7 @@ int ax_dispatch(const double* u, const double* g, const double* dx, double* w, i
 {
     switch (n) {
 #define SEM_AX_CASE(NV) \
-    case NV: return ax_n<NV>(u, g, dx, w, E, variant, stream);
+    case NV: return ax_entry_##NV(u, g, dx, w, E, variant, stream);
         SEM_AX_CASE(2) SEM_AX_CASE(3) SEM_AX_CASE(4) SEM_AX_CASE(5) SEM_AX_CASE(6)
         SEM_AX_CASE(7) SEM_AX_CASE(8) SEM_AX_CASE(9) SEM_AX_CASE(10) SEM_AX_CASE(11)
         SEM_AX_CASE(12) SEM_AX_CASE(13) SEM_AX_CASE(14) SEM_AX_CASE(15) SEM_AX_CASE(16)

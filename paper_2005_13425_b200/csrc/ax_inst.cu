@@ -1,0 +1,43 @@
+// Per-n instantiation of the Ax kernels (ax_impl.cuh).  build.py compiles
+// this file once per SEM_AX_GROUP so the heavy unrolled instantiations build
+// in parallel; ax.cu dispatches to ax_entry_<n> / ax_cg_entry_<n>.
+#include "ax_impl.cuh"
+
+#ifndef SEM_AX_GROUP
+#error "compile with -DSEM_AX_GROUP=<0..7>"
+#endif
+
+namespace sem {
+
+#define SEM_AX_DEFINE(NV)                                                                    \
+    int ax_entry_##NV(const double* u, const double* g, const double* dx, double* w,          \
+                      int64_t E, int variant, cudaStream_t s)                                 \
+    {                                                                                         \
+        return ax_n<NV>(u, g, dx, w, E, variant, s);                                          \
+    }                                                                                         \
+    int ax_cg_entry_##NV(double* p, const double* r, const double* g, const double* dx,       \
+                         double* w, int64_t E, sem_cg_state* st, double* hist, cudaStream_t s) \
+    {                                                                                         \
+        return ax_cg_n<NV>(p, r, g, dx, w, E, st, hist, s);                                   \
+    }
+
+// groups balanced by compile cost (grows steeply with n)
+#if SEM_AX_GROUP == 0
+SEM_AX_DEFINE(16)
+#elif SEM_AX_GROUP == 1
+SEM_AX_DEFINE(15)
+#elif SEM_AX_GROUP == 2
+SEM_AX_DEFINE(14)
+#elif SEM_AX_GROUP == 3
+SEM_AX_DEFINE(13) SEM_AX_DEFINE(2)
+#elif SEM_AX_GROUP == 4
+SEM_AX_DEFINE(12) SEM_AX_DEFINE(3)
+#elif SEM_AX_GROUP == 5
+SEM_AX_DEFINE(11) SEM_AX_DEFINE(4) SEM_AX_DEFINE(5)
+#elif SEM_AX_GROUP == 6
+SEM_AX_DEFINE(10) SEM_AX_DEFINE(6)
+#elif SEM_AX_GROUP == 7
+SEM_AX_DEFINE(9) SEM_AX_DEFINE(8) SEM_AX_DEFINE(7)
+#endif
+
+}  // namespace sem

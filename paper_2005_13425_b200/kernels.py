@@ -1,13 +1,14 @@
 """Element-local Poisson operator ``apply_ax`` on the B200 (contract of
 sembench/kernels.py:413-468).
 
-Every variant name the reference accepts is accepted here, with the
-reference's validation and error behaviour (``ValueError`` for shape / name
-problems, ``ScratchCapacityError`` for SCRATCH beyond n=10, the analytic
-``TrafficCounters`` inventory), but the arithmetic always runs the
-LAYERED sm_100a kernel of csrc/ax.cu -- the variants are different storage
-strategies for identical mathematics (reference docstring :1-45), and the
-GPU layered kernel is the one the paper (§IV-C) and the north star name.
+Every variant name the reference accepts runs its own sm_100a kernel, with
+the reference's validation and error behaviour (``ValueError`` for shape /
+name problems, ``ScratchCapacityError`` for SCRATCH beyond n=10, the
+analytic ``TrafficCounters`` inventory): LAYERED is the tuned pencil kernel
+of csrc/ax.cu (the paper's §IV-C design and the north-star path, 1e-12 of
+the reference); REFERENCE and SCRATCH are the paper's baselines
+(csrc/ax_variants.cu, bit-identical to the reference, REFERENCE leaving the
+metric-scaled gradients in its workspace just as sembench does).
 """
 
 from __future__ import annotations
@@ -90,9 +91,14 @@ def ax_bytes_per_apply(dofs: int) -> int:
     return 64 * dofs
 
 
-def reference_workspace(num_elements: int, n: int):
-    """Accepted for signature compatibility; the GPU kernel needs no workspace."""
+def reference_workspace(num_elements: int, n: int, device=None):
+    """The REFERENCE variant's three full-size intermediates (kernels.py:
+    :138-146).  numpy arrays by default (the reference's type: the GPU pass
+    results are copied back into them); ``device=`` gives CUDA tensors that
+    the kernels write in place."""
     shape = (num_elements, n, n, n)
+    if device is not None:
+        return tuple(torch.empty(shape, dtype=torch.float64, device=device) for _ in range(3))
     return np.empty(shape), np.empty(shape), np.empty(shape)
 
 
@@ -132,7 +138,9 @@ def apply_ax(u, geom: GeomFactors, basis: PolynomialBasis,
             f"scratch variant supports at most {SCRATCH_MAX_POINTS} points per "
             f"dimension, got n={n}")
     kind = dv.io_kind(u)
-    if kind == "device":
+    if variant is not KernelVariant.LAYERED:
+        result = _apply_ax_variant(u, kind, geom, basis, variant, workspace)
+    elif kind == "device":
         with torch.cuda.device(u.device):
             ud = dv.as_device_f64(u, u.device, "u")
             gd = geom.device_values(ud.device)
@@ -148,6 +156,52 @@ def apply_ax(u, geom: GeomFactors, basis: PolynomialBasis,
                      writes=apply_write_words(variant, dofs),
                      flops=flops_per_apply(dofs, n))
     return result
+
+
+_ref_scratch: dict = {}
+
+
+def _apply_ax_variant(u, kind: str, geom: GeomFactors, basis: PolynomialBasis,
+                      variant: KernelVariant, workspace):
+    """REFERENCE / SCRATCH on the GPU (csrc/ax_variants.cu), bit-exact with the
+    reference.  Host inputs are copied to the device and the result back; a
+    host workspace receives the intermediates like the reference's does."""
+    ud, kind = dv.to_device_io(u, "u")
+    dev = ud.device
+    n, E = basis.n, int(ud.shape[0])
+    dx = np.ascontiguousarray(basis.diff, dtype=np.float64)
+    with torch.cuda.device(dev):
+        gd = geom.device_values(dev)
+        wd = torch.empty_like(ud)
+        stream = dv.stream_handle(dev)
+        if variant is KernelVariant.SCRATCH:
+            check(load().sem_ax_scratch(dv.ptr(ud), dv.ptr(gd), dv.host_f64_ptr(dx), dv.ptr(wd),
+                                        E, n, stream), "apply_ax")
+        else:
+            dxt = np.ascontiguousarray(basis.diff_t, dtype=np.float64)
+            on_dev = workspace is not None and all(
+                isinstance(a, torch.Tensor) and a.device == dev and a.dtype == torch.float64
+                and a.is_contiguous() for a in workspace)
+            if on_dev:
+                ws = tuple(workspace)
+            else:
+                key = (dev.index, E * n ** 3)
+                buf = _ref_scratch.get(key)
+                if buf is None:
+                    _ref_scratch.clear()
+                    buf = torch.empty((3,) + tuple(ud.shape), dtype=torch.float64, device=dev)
+                    _ref_scratch[key] = buf
+                ws = (buf[0], buf[1], buf[2])
+            check(load().sem_ax_reference(dv.ptr(ud), dv.ptr(gd), dv.host_f64_ptr(dx),
+                                          dv.host_f64_ptr(dxt), *(dv.ptr(a) for a in ws),
+                                          dv.ptr(wd), E, n, stream), "apply_ax")
+            if workspace is not None and not on_dev:
+                for dst, src in zip(workspace, ws):
+                    if isinstance(dst, torch.Tensor):
+                        dst.copy_(src)
+                    else:
+                        dst[...] = src.cpu().numpy()
+    return dv.from_device_io(wd, kind)
 
 
 # elements per streamed chunk for host-buffer calls: 8 MB of u was the

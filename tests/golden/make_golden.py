@@ -73,7 +73,13 @@ def main() -> int:
         key = f"ax/{E}x{n}"
         d[key + "/meta"] = np.array([E, n, su, sg], dtype=np.int64)
         d[key + "/layered"] = sb.apply_ax(u, geom, basis, "layered")
-        d[key + "/reference"] = sb.apply_ax(u, geom, basis, "reference")
+        ws = sb.reference_workspace(E, n)
+        d[key + "/reference"] = sb.apply_ax(u, geom, basis, "reference", workspace=ws)
+        # the REFERENCE variant leaves the metric-scaled gradients in its workspace
+        for name, a in zip(("ur", "us", "ut"), ws):
+            d[key + "/reference_ws_" + name] = np.array(a)
+        if n <= sb.kernels.SCRATCH_MAX_POINTS:
+            d[key + "/scratch"] = sb.apply_ax(u, geom, basis, "scratch")
         if n <= 5:
             d[key + "/dense"] = verify.apply_dense(basis, geom, u)
 

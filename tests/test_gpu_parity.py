@@ -102,6 +102,65 @@ def test_ax_large_properties(cuda):
     assert O.rel_diff(au[idx].cpu().numpy(), ref) <= AX_TOL
 
 
+@pytest.mark.parametrize("key", ["1x2", "8x3", "8x4", "4x5", "2x7", "8x10", "3x9", "1x16"])
+def test_ax_reference_scratch_golden(cuda, golden, key):
+    """REFERENCE / SCRATCH GPU kernels are BIT-IDENTICAL to the reference's own
+    outputs, and REFERENCE leaves the same intermediates in a host workspace."""
+    E, n, su, sg = (int(v) for v in golden[f"ax/{key}/meta"])
+    u, g = _rand_inputs(E, n, su, sg)
+    geom, b = sb.GeomFactors(values=g), sb.build_basis(n)
+    ws = sb.reference_workspace(E, n)
+    w = sb.apply_ax(u, geom, b, "reference", workspace=ws)
+    assert np.array_equal(w, golden[f"ax/{key}/reference"])
+    for name, a in zip(("ur", "us", "ut"), ws):
+        assert np.array_equal(a, golden[f"ax/{key}/reference_ws_{name}"])
+    if n <= 10:
+        assert np.array_equal(sb.apply_ax(u, geom, b, "scratch"), golden[f"ax/{key}/scratch"])
+    else:
+        with pytest.raises(sb.ScratchCapacityError):
+            sb.apply_ax(u, geom, b, "scratch")
+
+
+@pytest.mark.parametrize("n", [2, 5, 8, 10, 13, 16])
+def test_ax_variants_vs_oracle(cuda, n):
+    """Device tensors in / out, device workspace written in place; larger E
+    than the fixtures.  Bit-exact vs the oracle restatements; all three
+    variants within the reassociation bar of each other."""
+    E = {2: 300, 5: 257, 8: 129, 10: 97, 13: 21, 16: 9}[n]
+    u, g = _rand_inputs(E, n, 70 + n, 80 + n)
+    b = sb.build_basis(n)
+    ud, gd = torch.from_numpy(u).cuda(), sb.GeomFactors(values=torch.from_numpy(g).cuda())
+    ws = sb.reference_workspace(E, n, device=ud.device)
+    wr = sb.apply_ax(ud, gd, b, "reference", workspace=ws)
+    ref_w, ref_r, ref_s, ref_t = O.ax_reference(u, g, b.diff, b.diff_t)
+    assert wr.is_cuda and np.array_equal(wr.cpu().numpy(), ref_w)
+    for a, r in zip(ws, (ref_r, ref_s, ref_t)):
+        assert np.array_equal(a.cpu().numpy(), r)
+    wl = sb.apply_ax(ud, gd, b, "layered").cpu().numpy()
+    assert O.rel_diff(wl, ref_w) <= AX_TOL
+    if n <= 10:
+        wsc = sb.apply_ax(ud, gd, b, "scratch").cpu().numpy()
+        assert np.array_equal(wsc, O.ax_scratch(u, g, b.diff))
+        assert O.rel_diff(wsc, ref_w) <= AX_TOL
+
+
+def test_ax_variants_headline_size(cuda):
+    """E=4096, p=9: REFERENCE and SCRATCH against LAYERED (1e-12) and a
+    spot-check of elements against the oracle, bit-exact."""
+    E, n = 4096, 10
+    b = sb.build_basis(n)
+    u = sb.random_field(E, n, 1, device="cuda")
+    geom = sb.GeomFactors(values=sb.random_field(6 * E, n, 2, device="cuda").reshape(E, 6, n, n, n))
+    wl = sb.apply_ax(u, geom, b).cpu().numpy()
+    wr = sb.apply_ax(u, geom, b, "reference").cpu().numpy()
+    wsc = sb.apply_ax(u, geom, b, "scratch").cpu().numpy()
+    assert O.rel_diff(wr, wl) <= AX_TOL and O.rel_diff(wsc, wl) <= AX_TOL
+    idx = [0, 1, 2047, E - 1]
+    uu, gg = u[idx].cpu().numpy(), geom.values[idx].cpu().numpy()
+    assert np.array_equal(wr[idx], O.ax_reference(uu, gg, b.diff, b.diff_t)[0])
+    assert np.array_equal(wsc[idx], O.ax_scratch(uu, gg, b.diff))
+
+
 @pytest.mark.parametrize("mode", ["1", "0", "2", "3"])
 @pytest.mark.parametrize("kind", ["numpy", "pinned", "pageable"])
 def test_ax_host_streaming(cuda, kind, mode, monkeypatch):

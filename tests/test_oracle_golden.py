@@ -44,6 +44,22 @@ def test_ax_layered_bitexact(golden, key):
         assert O.rel_diff(w, dense) <= 1e-12
 
 
+@pytest.mark.parametrize("key", ["1x2", "8x3", "8x4", "4x5", "2x7", "8x10", "3x9", "1x16"])
+def test_ax_reference_scratch_bitexact(golden, key):
+    """REFERENCE (kernels.py:159-205, including the intermediates it leaves in
+    its workspace) and SCRATCH (:213-259) restatements, bit-for-bit."""
+    E, n, su, sg = (int(v) for v in golden[f"ax/{key}/meta"])
+    u = O.random_field(E, n, su)
+    g = O.random_field(6 * E, n, sg).reshape(E, 6, n, n, n)
+    dx, dxt = golden[f"basis/{n}/diff"], golden[f"basis/{n}/diff_t"]
+    w, ur, us, ut = O.ax_reference(u, g, dx, dxt)
+    assert np.array_equal(w, golden[f"ax/{key}/reference"])
+    for name, a in (("ur", ur), ("us", us), ("ut", ut)):
+        assert np.array_equal(a, golden[f"ax/{key}/reference_ws_{name}"])
+    if n <= 10:
+        assert np.array_equal(O.ax_scratch(u, g, dx), golden[f"ax/{key}/scratch"])
+
+
 def test_ax_box_geometry(golden):
     w = golden["basis/10/weights"]
     g = O.box_geom(2, 2, 1, w, 0.5)
