@@ -27,6 +27,7 @@
  *   sem_cg_*           cg.py:114-193 cg_solve loop (device-resident scalars)
  *   sem_random_field   fields.py:42-54 random_field (bit-exact SplitMix64)
  *   sem_box_geom       mesh.py:72-91 build_geom (bit-exact)
+ *   sem_stream_copy    perf.py:156-159 _stream_copy (bandwidth probe)
  */
 #ifndef SEM_H_
 #define SEM_H_
@@ -153,6 +154,14 @@ int sem_cg_run(const double *g, const double *dx, const double *dxt, double *x,
                double *r, double *p, double *w, sem_cg_state *state, double *history,
                int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,
                void *scratch, sem_stream_t stream);
+/* sem_cg_run with CUDA events between its launches (measurement only):
+ * synchronises, then ADDS each phase's device milliseconds to phase_ms[0]
+ * (Ax with the fused p update), [1] (dssum + mask + <p,w>), [2] (x, r
+ * updates + <r,r>). */
+int sem_cg_run_phases(const double *g, const double *dx, const double *dxt, double *x,
+                      double *r, double *p, double *w, sem_cg_state *state, double *history,
+                      int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+                      void *scratch, double *phase_ms, sem_stream_t stream);
 
 /* ------------------------------------------- multi-GPU z-slab partition -- */
 /* A rank owns global element layers [gz0, gz0+ez) of an ex*ey*ez_global box
@@ -210,6 +219,11 @@ int sem_random_field(double *out, int64_t count, uint64_t seed, sem_stream_t str
  * weights is a HOST array of n GLL weights. */
 int sem_box_geom(double *g, int64_t num_elements, int32_t n, const double *weights,
                  double extent, sem_stream_t stream);
+
+/* ------------------------------------------------------------ probe ---- */
+/* dst[i] = src[i] for count doubles (device, non-overlapping): the streaming
+ * copy that measure_bandwidth times (perf.py:156-203, paper §V). */
+int sem_stream_copy(double *dst, const double *src, int64_t count, sem_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -70,6 +70,8 @@ SIGNATURES = {
                                    _i32, _vp, _vp]),
     "sem_cg_run": (ctypes.c_int, [_vp, _dp, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,
                                   _i32, _i32, _vp, _vp]),
+    "sem_cg_run_phases": (ctypes.c_int, [_vp, _dp, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
+                                         _i32, _i32, _i32, _vp, _dp, _vp]),
     "sem_slab_plane_top": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp]),
     "sem_slab_plane_bottom": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
     "sem_dssum_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
@@ -88,6 +90,7 @@ SIGNATURES = {
     "sem_cg_finish": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
     "sem_random_field": (ctypes.c_int, [_vp, _i64, ctypes.c_uint64, _vp]),
     "sem_box_geom": (ctypes.c_int, [_vp, _i64, _i32, _dp, _f64, _vp]),
+    "sem_stream_copy": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
 }
 
 _lib = None

@@ -18,7 +18,7 @@ OUT = os.path.join(HERE, "libsem.so")
 # ax_inst.cu is compiled once per n group (-DSEM_AX_GROUP=k) so the unrolled
 # per-n Ax instantiations build in parallel.
 AX_GROUPS = 8
-SOURCES = ["common.cu", "ax.cu", "ax_variants.cu", "assembly.cu", "cg.cu", "fields.cu", "host.cu", "slab.cu"]
+SOURCES = ["common.cu", "ax.cu", "ax_variants.cu", "assembly.cu", "cg.cu", "fields.cu", "host.cu", "slab.cu", "probe.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -31,7 +31,7 @@ from .fields import validate_field
 from .kernels import TrafficCounters
 
 __all__ = ["CgConfig", "CgResult", "CgBreakdownError", "weighted_dot", "cg_solve",
-           "CG_VECTOR_FLOPS_PER_POINT", "CgWorkspace"]
+           "CG_VECTOR_FLOPS_PER_POINT", "CgWorkspace", "fused_phase_seconds"]
 
 CG_VECTOR_FLOPS_PER_POINT = 12
 USE_GRAPHS = True  # replay one captured iteration (fused path)
@@ -183,6 +183,37 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
     zero_exit = st.stop == 1
     solution = ws.x.clone()
     return solution, history, iters, zero_exit
+
+
+def fused_phase_seconds(f, op: GlobalOperator, topo: Topology, iterations: int,
+                        workspace: CgWorkspace | None = None) -> tuple[float, float, float]:
+    """Device seconds of the fused solve's three phases over `iterations`
+    eagerly launched iterations (sem_cg_run_phases: CUDA events between the
+    launches): (Ax with the fused p update, assemble = dssum + mask + <p,w>,
+    x/r updates + <r,r>).  Measurement helper for harness.py; the solve's
+    result is discarded."""
+    import ctypes
+    lib = load()
+    fd = dv.as_device_f64(f, None, "f")
+    dev = fd.device
+    ws = workspace
+    if ws is None or ws.max_iterations < iterations or ws.device != dev:
+        ws = CgWorkspace(topo, iterations, dev)
+    box = (topo.ex, topo.ey, topo.ez, topo.n)
+    g = op.geom.device_values(dev)
+    dx = np.ascontiguousarray(op.basis.diff, dtype=np.float64)
+    dxt = np.ascontiguousarray(op.basis.diff_t, dtype=np.float64)
+    ms = (ctypes.c_double * 3)(0.0, 0.0, 0.0)
+    with torch.cuda.device(dev):
+        s = dv.stream_handle(dev)
+        check(lib.sem_cg_init(dv.ptr(fd), dv.ptr(ws.x), dv.ptr(ws.r), dv.ptr(ws.p),
+                              dv.ptr(ws.state), dv.ptr(ws.history), iterations, 0.0, *box,
+                              dv.ptr(ws.scratch), s), "cg_solve init")
+        check(lib.sem_cg_run_phases(dv.ptr(g), dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt),
+                                    dv.ptr(ws.x), dv.ptr(ws.r), dv.ptr(ws.p), dv.ptr(ws.w),
+                                    dv.ptr(ws.state), dv.ptr(ws.history), iterations, *box,
+                                    dv.ptr(ws.scratch), ms, s), "cg phase timing")
+    return ms[0] * 1e-3, ms[1] * 1e-3, ms[2] * 1e-3
 
 
 def _generic_solve(f_dev: torch.Tensor, operator, topo: Topology, cfg: CgConfig, counters,

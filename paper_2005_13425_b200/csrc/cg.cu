@@ -311,18 +311,26 @@ static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_st
 template <int N>
 static int cg_run_n(const double* g, const double* dx, double* x, double* r, double* p,
                     double* w, double* w2, sem_cg_state* st, double* history, int iters,
-                    int64_t E, Box bx, ReduceScratch* rs, cudaStream_t s)
+                    int64_t E, Box bx, ReduceScratch* rs, cudaStream_t s,
+                    cudaEvent_t* marks = nullptr)
 {
+    // marks (optional, 3*iters+1 events): recorded before each iteration's
+    // Ax, assemble and update launches and after the last one
+    auto mark = [&](int q) { return marks ? cudaEventRecord(marks[q], s) : cudaSuccess; };
     for (int it = 0; it < iters; ++it) {
+        if (cudaError_t e = mark(3 * it)) return fail_cuda(e, "sem_cg_run: event");
         // p = beta p + r fused into the Ax prologue (ax_pencil.cuh, CGP)
         if (int rc = ax_cg_dispatch(p, r, g, dx, w, E, N, st, history, s)) return rc;
+        if (cudaError_t e = mark(3 * it + 1)) return fail_cuda(e, "sem_cg_run: event");
         cg_assemble_kernel<N, false><<<row_grid<N>(E), kRowThreads, 0, s>>>(w, w2, p, E, bx, st,
                                                                              rs, nullptr, nullptr);
         SEM_CHECK_LAUNCH("cg_assemble_kernel");
+        if (cudaError_t e = mark(3 * it + 2)) return fail_cuda(e, "sem_cg_run: event");
         cg_update_kernel<N, false><<<red_grid<N>(E), PairCfg<N>::THREADS, 0, s>>>(x, r, p, w2, E, make_box_flat(bx),
                                                                            st, history, rs);
         SEM_CHECK_LAUNCH("cg_update_kernel");
     }
+    if (cudaError_t e = mark(3 * iters)) return fail_cuda(e, "sem_cg_run: event");
     return 0;
 }
 
@@ -431,6 +439,55 @@ extern "C" int sem_cg_run(const double* g, const double* dx, const double* dxt, 
     double* w_asm = w + m;
     SEM_SWITCH_N(n, return cg_run_n<NV>(g, dx, x, r, p, w_local, w_asm, state, history,
                                         iterations, E, bx, rs, s));
+}
+
+// Instrumented form of sem_cg_run: the same launches, eagerly, with CUDA
+// events between them; synchronises and adds each phase's device time (ms)
+// to phase_ms[0] (Ax incl. the fused p update), [1] (assemble: dssum + mask
+// + <p,w>), [2] (x/r updates + <r,r>).  Measurement only (harness.py).
+extern "C" int sem_cg_run_phases(const double* g, const double* dx, const double* dxt, double* x,
+                                 double* r, double* p, double* w, sem_cg_state* state,
+                                 double* history, int32_t iterations, int32_t ex, int32_t ey,
+                                 int32_t ez, int32_t n, void* scratch, double* phase_ms,
+                                 sem_stream_t stream)
+{
+    (void)dxt;
+    if (int rc = check_box(ex, ey, ez, n, "sem_cg_run_phases")) return rc;
+    if (!g || !dx || !x || !r || !p || !w || !state || !history || !scratch || !phase_ms ||
+        iterations < 0 || iterations > 100000) {
+        set_error("sem_cg_run_phases: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const Box bx{ex, ey, ez, 0, ez};
+    const int64_t E = (int64_t)ex * ey * ez;
+    const int64_t m = E * n * n * n;
+    auto* rs = static_cast<ReduceScratch*>(scratch);
+    const int nev = 3 * iterations + 1;
+    cudaEvent_t* marks = new cudaEvent_t[nev];
+    int made = 0, rc = 0;
+    cudaError_t err = cudaSuccess;
+    for (; made < nev && err == cudaSuccess; ++made) err = cudaEventCreate(&marks[made]);
+    if (err != cudaSuccess) {
+        --made;
+        rc = fail_cuda(err, "sem_cg_run_phases: events");
+    }
+    if (rc == 0) {
+        SEM_SWITCH_N(n, rc = cg_run_n<NV>(g, dx, x, r, p, w, w + m, state, history, iterations, E,
+                                          bx, rs, s, marks); break);
+    }
+    if (rc == 0 && (err = cudaEventSynchronize(marks[nev - 1])) != cudaSuccess)
+        rc = fail_cuda(err, "sem_cg_run_phases: sync");
+    for (int q = 0; rc == 0 && q < nev - 1; ++q) {
+        float ms = 0.f;
+        if ((err = cudaEventElapsedTime(&ms, marks[q], marks[q + 1])) != cudaSuccess)
+            rc = fail_cuda(err, "sem_cg_run_phases: elapsed");
+        phase_ms[q % 3] += ms;
+    }
+    for (int q = 0; q < made; ++q) cudaEventDestroy(marks[q]);
+    delete[] marks;
+    return rc;
 }
 
 // ------------------------------------------------- multi-GPU (z-slab) CG --

@@ -9,13 +9,14 @@ bytes (u 8 + g 48 + w 8 per point).
 
 from __future__ import annotations
 
+import ctypes
 import json
 import os
 from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["model_flops_per_iteration", "model_bytes_per_iteration",
+__all__ = ["measure_bandwidth", "B200_L2_BYTES", "model_flops_per_iteration", "model_bytes_per_iteration",
            "model_read_bytes_per_iteration", "model_write_bytes_per_iteration", "intensity",
            "roofline_peak", "probe_byte_accounting", "evaluate_roofline", "RooflineResult",
            "CostModel", "CACHE_EFFECT_THRESHOLD", "LLC_WARN_BYTES", "ax_intensity",
@@ -120,6 +121,75 @@ def evaluate_roofline(run_flops: int, run_seconds: float, bandwidth: float, n: i
     flags = ("cache-effect",) if frac > CACHE_EFFECT_THRESHOLD else ()
     return RooflineResult(measured_bandwidth=bandwidth, intensity=intensity(n),
                           peak_flops=peak, achieved_flops=achieved, fraction=frac, flags=flags)
+
+
+_MIN_REPETITIONS = 10
+# The reference's 1 ms floor guards a host perf_counter; CUDA events resolve
+# ~0.5 us, so the device probe's floor is 20 us of timed copies (40x the
+# event resolution) -- a 64-element probe (15 MB) takes ~0.1 ms for 10 reps.
+_MIN_ELAPSED_SECONDS = 2e-5
+# B200 L2 (126 MB): a probe payload below it streams partly from L2, so the
+# GPU analog of the reference's last-level-cache warning uses the larger of
+# the two thresholds.
+B200_L2_BYTES = 126 * 1024 * 1024
+
+
+def measure_bandwidth(dofs: int, repetitions: int = 10, warmup: int = 2, device=None) -> float:
+    """Device streaming-copy bandwidth in bytes/second at the model's buffer
+    size (the contract of sembench/perf.py:162-203 on the GPU).
+
+    Allocates a source and a destination of 240 D bytes each in HBM, copies
+    source to destination once per repetition with the library's streaming
+    copy kernel (sem_stream_copy), times each repetition with CUDA events and
+    reports the median rate counting read plus write streams.  Warm-up
+    repetitions are excluded.  Same errors as the reference: ValueError for
+    fewer than 10 repetitions, RuntimeWarning when the payload may fit in
+    cache, MemoryError when the buffers cannot be allocated, RuntimeError when
+    the timed region is below timer resolution.
+    """
+    import warnings
+
+    import torch
+
+    from . import _device as dv
+    from ._lib import check, load
+
+    if repetitions < _MIN_REPETITIONS:
+        raise ValueError(f"repetitions must be at least {_MIN_REPETITIONS}, got {repetitions}")
+    payload, counted = probe_byte_accounting(dofs)
+    limit = max(LLC_WARN_BYTES, B200_L2_BYTES)
+    if payload < limit:
+        warnings.warn(f"probe payload {payload} bytes may fit in cache (below {limit}); "
+                      "bandwidth may read high", RuntimeWarning, stacklevel=2)
+    dev = torch.device(device) if device is not None else dv.current_device()
+    nwords = payload // WORD_BYTES
+    try:
+        src = torch.ones(nwords, dtype=torch.float64, device=dev)
+        dst = torch.empty(nwords, dtype=torch.float64, device=dev)
+    except torch.OutOfMemoryError as exc:
+        raise MemoryError(f"cannot allocate two {payload}-byte probe buffers") from exc
+    lib = load()
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        handle = ctypes.c_void_p(stream.cuda_stream)
+
+        def copy():
+            check(lib.sem_stream_copy(dv.ptr(dst), dv.ptr(src), nwords, handle), "measure_bandwidth")
+
+        for _ in range(max(warmup, 1)):
+            copy()
+        events = [torch.cuda.Event(enable_timing=True) for _ in range(repetitions + 1)]
+        events[0].record(stream)
+        for rep in range(repetitions):
+            copy()
+            events[rep + 1].record(stream)
+        events[-1].synchronize()
+    times = np.array([events[r].elapsed_time(events[r + 1]) * 1e-3 for r in range(repetitions)])
+    if times.sum() < _MIN_ELAPSED_SECONDS:
+        raise RuntimeError(f"probe finished in {times.sum():.2e} s, below timer resolution; "
+                           "increase repetitions or the problem size")
+    rates = np.where(times > 0.0, counted / np.maximum(times, 1e-300), np.inf)
+    return float(np.median(rates))
 
 
 _FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when the driver file is absent

@@ -135,6 +135,46 @@ def main() -> int:
     d["factor/counts"] = np.array(FACTOR_COUNTS, dtype=np.int64)
     d["factor/boxes"] = np.array([sb.factor_elements(c) for c in FACTOR_COUNTS], dtype=np.int64)
 
+    # report serialisations emitted by the reference (sembench-1 schema)
+    from sembench import report as R
+    rows = []
+    for q, (variant, elements) in enumerate([("reference", 64), ("scratch", 64), ("layered", 64),
+                                             ("layered", 4096), ("reference", 4096)]):
+        rows.append(R.PerfReport(
+            schema_version=R.SCHEMA_VERSION, variant=variant, elements=elements,
+            box="4x4x4" if elements == 64 else "16x16x16", n=10, dofs=elements * 1000,
+            iterations=100, workers=148, seed=1, include_dssum=(q % 2 == 1),
+            total_seconds=0.1 + q / 3.0, seconds_per_iteration=(0.1 + q / 3.0) / 100,
+            ax_seconds=1e-3 * (q + 1) / 7.0, dssum_seconds=2.5e-4 / (q + 3),
+            model_flops_per_iteration=elements * 1000 * 154,
+            model_bytes_per_iteration=elements * 1000 * 240,
+            model_read_bytes_per_iteration=elements * 1000 * 192,
+            model_write_bytes_per_iteration=elements * 1000 * 48,
+            instr_flops=elements * 1000 * 147 * 100, instr_read_words=elements * 1000 * 36 * 100,
+            instr_write_words=elements * 1000 * 8 * 100, achieved_gflops=5303.914826095655 / (q + 1),
+            measured_bandwidth=6.0931e12 + q, roofline_peak_gflops=3909.8 + q / 10.0,
+            roofline_fraction=1.2616330551493 / (q + 1),
+            flags="" if q < 2 else ("probe-under-llc" if q < 4 else "probe-under-llc;cache-effect")))
+    # deterministic integer fields of the reference's own benchmark rows
+    # (traffic / flop inventory of a 10-iteration solve, every variant)
+    sb.set_workers(2)
+    bench_rows = sb.run_bench(sb.BenchConfig(elements=64, iterations=10, variant="all",
+                                             probe_repetitions=10))
+    int_fields = ["elements", "n", "dofs", "iterations", "seed", "model_flops_per_iteration",
+                  "model_bytes_per_iteration", "model_read_bytes_per_iteration",
+                  "model_write_bytes_per_iteration", "instr_flops", "instr_read_words",
+                  "instr_write_words"]
+    d["bench64/int_fields"] = np.frombuffer(",".join(int_fields).encode(), dtype=np.uint8)
+    d["bench64/variants"] = np.frombuffer(",".join(r.variant for r in bench_rows).encode(),
+                                          dtype=np.uint8)
+    d["bench64/values"] = np.array([[getattr(r, k) for k in int_fields] for r in bench_rows],
+                                   dtype=np.int64)
+    d["bench64/roofline_keys"] = np.frombuffer(
+        ",".join(sb.run_roofline(sb.BenchConfig(elements=64)).keys()).encode(), dtype=np.uint8)
+    for fmt, text in (("csv", R.emit_csv(rows)), ("json", R.emit_json(rows)),
+                      ("gnuplot", R.emit_gnuplot(rows))):
+        d[f"report/{fmt}"] = np.frombuffer(text.encode(), dtype=np.uint8)
+
     np.savez_compressed(OUT, **d)
     print(f"wrote {OUT}: {len(d)} arrays, {os.path.getsize(OUT)} bytes")
     return 0
