@@ -139,7 +139,8 @@ typedef struct sem_cg_state {
     int32_t stop;      /* 0 running, 1 exact zero residual (cg.py:151),
                           2 breakdown <p,Ap> <= 0, 3 tolerance reached */
     int32_t breakdown_it;
-    int32_t pad_;
+    int32_t x_pending; /* single GPU: x += alpha p of the last completed
+                          iteration not yet applied (sem_cg_finalize)     */
     double local_sum;  /* multi-GPU: this rank's partial of the last reduction */
 } sem_cg_state;
 
@@ -148,16 +149,23 @@ int sem_cg_init(const double *f, double *x, double *r, double *p, sem_cg_state *
                 double *history, int32_t max_iterations, double tolerance,
                 int32_t ex, int32_t ey, int32_t ez, int32_t n, void *scratch,
                 sem_stream_t stream);
-/* Enqueue `iterations` fused CG iterations on the box operator (single GPU).
- * w is a 2*E*n^3 scratch buffer; history receives sqrt(<r,r>_c) per iteration. */
+/* Enqueue `iterations` fused CG iterations on the box operator (single GPU):
+ * two launches per iteration (Ax with the iteration head, x update and
+ * <p,Ap> fused; r update with dssum + mask fused).  w is a 2*E*n^3 scratch
+ * buffer; history receives sqrt(<r,r>_c) per iteration.  The x update of
+ * the LAST iteration run is deferred: call sem_cg_finalize before reading x. */
 int sem_cg_run(const double *g, const double *dx, const double *dxt, double *x,
                double *r, double *p, double *w, sem_cg_state *state, double *history,
                int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,
                void *scratch, sem_stream_t stream);
+/* Apply the pending x += alpha p (if any; not after a breakdown) and clear it.
+ * num_points = E*n^3. */
+int sem_cg_finalize(double *x, const double *p, sem_cg_state *state, int64_t num_points,
+                    sem_stream_t stream);
 /* sem_cg_run with CUDA events between its launches (measurement only):
  * synchronises, then ADDS each phase's device milliseconds to phase_ms[0]
- * (Ax with the fused p update), [1] (dssum + mask + <p,w>), [2] (x, r
- * updates + <r,r>). */
+ * (Ax with the fused iteration head and <p,Ap>), [1] (r update with the
+ * fused dssum + mask, <r,r>), [2] (unused). */
 int sem_cg_run_phases(const double *g, const double *dx, const double *dxt, double *x,
                       double *r, double *p, double *w, sem_cg_state *state, double *history,
                       int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,

@@ -33,7 +33,7 @@ class sem_cg_state(ctypes.Structure):
         ("iterations_run", ctypes.c_int32),
         ("stop", ctypes.c_int32),
         ("breakdown_it", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("x_pending", ctypes.c_int32),
         ("local_sum", ctypes.c_double),
     ]
 
@@ -70,6 +70,7 @@ SIGNATURES = {
                                    _i32, _vp, _vp]),
     "sem_cg_run": (ctypes.c_int, [_vp, _dp, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,
                                   _i32, _i32, _vp, _vp]),
+    "sem_cg_finalize": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "sem_cg_run_phases": (ctypes.c_int, [_vp, _dp, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
                                          _i32, _i32, _i32, _vp, _dp, _vp]),
     "sem_slab_plane_top": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp]),

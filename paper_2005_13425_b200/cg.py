@@ -148,6 +148,12 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
                              dv.ptr(ws.history), k, *box, dv.ptr(ws.scratch),
                              dv.stream_handle(dev)), "cg_solve run")
 
+    m = ws.x.numel()
+
+    def finalize():  # the deferred x += alpha p of the last iteration run
+        check(lib.sem_cg_finalize(dv.ptr(ws.x), dv.ptr(ws.p), dv.ptr(ws.state), m,
+                                  dv.stream_handle(dev)), "cg_solve finalize")
+
     if callback is None:
         if cfg.max_iterations > 2 and USE_GRAPHS:
             # iteration 1 launched directly (configures the kernels), then one
@@ -161,11 +167,13 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
                 graph.replay()
         else:
             run(cfg.max_iterations)
+        finalize()
         st = ws.read_state()
     else:
         st = None
         for it in range(1, cfg.max_iterations + 1):
             run(1)
+            finalize()
             st = ws.read_state()
             if st.iterations_run >= it and st.stop != 2:
                 x = dv.to_numpy(ws.x) if host else ws.x

@@ -3,26 +3,29 @@
 // instantiated per n in ax_inst.cu.
 #include "sem_common.cuh"
 #include "box.cuh"
+#include "ax_pencil.cuh"
 
 namespace sem {
 
 #define SEM_AX_DECLARE(NV)                                                                   \
     int ax_entry_##NV(const double* u, const double* g, const double* dx, double* w,          \
                       int64_t E, int variant, cudaStream_t s);                                \
-    int ax_cg_entry_##NV(double* p, const double* r, const double* g, const double* dx,       \
-                         double* w, int64_t E, sem_cg_state* st, double* hist, cudaStream_t s);
+    int ax_cg_entry_##NV(const double* g, const double* dx, double* w, int64_t E,             \
+                         CgpArgs a, int mode, cudaStream_t s);
 SEM_AX_DECLARE(2) SEM_AX_DECLARE(3) SEM_AX_DECLARE(4) SEM_AX_DECLARE(5) SEM_AX_DECLARE(6)
 SEM_AX_DECLARE(7) SEM_AX_DECLARE(8) SEM_AX_DECLARE(9) SEM_AX_DECLARE(10) SEM_AX_DECLARE(11)
 SEM_AX_DECLARE(12) SEM_AX_DECLARE(13) SEM_AX_DECLARE(14) SEM_AX_DECLARE(15) SEM_AX_DECLARE(16)
 #undef SEM_AX_DECLARE
 
-int ax_cg_dispatch(double* p, const double* r, const double* g, const double* dx, double* w,
-                   int64_t E, int n, sem_cg_state* st, double* hist, cudaStream_t stream)
+// mode 1: p-update prologue only (multi-GPU slab solver); mode 2: also the
+// deferred x update and <p, A p> -> alpha (single-GPU solver)
+int ax_cg_dispatch(const double* g, const double* dx, double* w, int64_t E, int n, CgpArgs a,
+                   int mode, cudaStream_t stream)
 {
     if (E == 0) return 0;
     switch (n) {
 #define SEM_AXCG_CASE(NV) \
-    case NV: return ax_cg_entry_##NV(p, r, g, dx, w, E, st, hist, stream);
+    case NV: return ax_cg_entry_##NV(g, dx, w, E, a, mode, stream);
         SEM_AXCG_CASE(2) SEM_AXCG_CASE(3) SEM_AXCG_CASE(4) SEM_AXCG_CASE(5) SEM_AXCG_CASE(6)
         SEM_AXCG_CASE(7) SEM_AXCG_CASE(8) SEM_AXCG_CASE(9) SEM_AXCG_CASE(10) SEM_AXCG_CASE(11)
         SEM_AXCG_CASE(12) SEM_AXCG_CASE(13) SEM_AXCG_CASE(14) SEM_AXCG_CASE(15) SEM_AXCG_CASE(16)
@@ -73,5 +76,5 @@ extern "C" int sem_ax(const double* u, const double* g, const double* dx,
 
 extern "C" int sem_ax_num_variants(int32_t n)
 {
-    return (n >= 2 && n <= 16) ? 40 : 0;
+    return (n >= 2 && n <= 16) ? 42 : 0;
 }

@@ -307,7 +307,7 @@ static bool fill_dparam(DParamP<N>& P, const double* dx)
 }
 
 template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
-          bool FOLD = false, bool CGP = false>
+          bool FOLD = false, int CGM = 0>
 static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
                          int64_t E, cudaStream_t stream, CgpArgs cgp = CgpArgs{})
 {
@@ -320,11 +320,11 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     const bool antisym = fill_dparam<N>(D, dx);
     if constexpr (FOLD) {
         if (!antisym)  // the even-odd form needs a centro-antisymmetric D
-            return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, false, CGP>(
+            return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, false, CGM>(
                 u, g, dx, w, E, stream, cgp);
     }
     if (E == 0) return 0;
-    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGP>;
+    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGM>;
     static bool configured = false;  // per template instance
     if (!configured) {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -352,17 +352,17 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
 }
 
 template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
-          bool FOLD = false, bool CGP = false>
+          bool FOLD = false, int CGM = 0>
 static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
                       cudaStream_t stream, CgpArgs cgp = CgpArgs{})
 {
     if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 && (GMODE != 2 || N % 2 == 0) &&
                   sizeof(double) * ((size_t)SLOTS * PencilCfg<N>::SLOT_DOUBLES +
                                     (GMODE ? (size_t)SLOTS * 6 * N * N * N + 6 : 0)) * MINB <= 227 * 1024)
-        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGP>(u, g, dx, w, E,
+        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGM>(u, g, dx, w, E,
                                                                                stream, cgp);
     else
-        return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, CGP>(
+        return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, CGM>(
             u, g, dx, w, E, stream, cgp);
 }
 
@@ -372,7 +372,7 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 // prefetch depth, persistent, L2 bulk prefetch>.
 // Default tuning point per n (tools/ax_sweep.py on B200, E=4096; see
 // profiles/r01_ax_sweep.txt, CUDA-graph timed): index = n, value = variant id.
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 37, 34, 34, 35, 5, 8, 7, 17, 3};
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 5, 8, 7, 17, 3};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
@@ -403,6 +403,9 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
         case 37: return try_pencil<N, 1, 4, false, 1, false, 1, true>(u, g, dx, w, E, stream);
         case 38: return try_pencil<N, 1, 3, false, 1, false, 2, true>(u, g, dx, w, E, stream);
         case 39: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 1, true>(u, g, dx, w, E, stream);
+        // + bulk L2 prefetch of the element a resident wave ahead
+        case 40: return try_pencil<N, 1, 3, false, 1, true, 1, true>(u, g, dx, w, E, stream);
+        case 41: return try_pencil<N, 1, 2, false, 1, true, 1, true>(u, g, dx, w, E, stream);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
@@ -428,19 +431,41 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
 
 // CG iteration head fused with Ax (p = beta p + r; w = A_local p): the tuned
 // configuration of each n with the metric staged by TMA and u through
-// registers (the p update happens while the column is loaded).
-template <int N>
-static int ax_cg_n(double* p, const double* r, const double* g, const double* dx, double* w,
-                   int64_t E, sem_cg_state* st, double* hist, cudaStream_t s)
+// registers (the p update happens while the column is loaded).  CGM = 1:
+// multi-GPU slab solver; CGM = 2: single-GPU solver (x update and <p,Ap>
+// fused too, see ax_pencil.cuh).
+template <int N, int CGM>
+static int ax_cg_n(const double* g, const double* dx, double* w, int64_t E, CgpArgs a,
+                   cudaStream_t s)
 {
-    const CgpArgs a{p, r, st, hist};
+    double* p = a.p;
+    if constexpr (N >= 8 && N <= 11) {
+        // tuning hook (SEM_CG_AX_CFG, tools/cg_phases.py): alternative
+        // tilings of the fused CG Ax for the headline degrees
+        static const int cfg = getenv("SEM_CG_AX_CFG") ? atoi(getenv("SEM_CG_AX_CFG")) : 0;
+        switch (cfg) {
+            case 1: return try_pencil<N, 1, 4, false, 1, false, 0, true, CGM>(p, g, dx, w, E, s, a);
+            case 2: return try_pencil<N, 1, 5, false, 2, false, 0, true, CGM>(p, g, dx, w, E, s, a);
+            case 3: return try_pencil<N, 2, 2, false, 1, false, 0, true, CGM>(p, g, dx, w, E, s, a);
+            case 4: return try_pencil<N, 1, 3, false, 1, false, 1, true, CGM>(p, g, dx, w, E, s, a);
+            case 5: return try_pencil<N, 1, 2, false, 1, false, 1, true, CGM>(p, g, dx, w, E, s, a);
+            default: break;
+        }
+    }
+    // default: TMA-staged metric, folded contractions, and a bulk L2 prefetch
+    // of the element that replaces this one on its SM (its g, p, r and x):
+    // the CG prologue reads three fields besides g, and warming L2 a wave
+    // ahead cut the fused Ax from 88 to 79 us at E = 4096 and from 608 to
+    // 502 us at E = 32768 (tools/cg_tune.sh, profiles/r01_cg_tune.txt)
     if constexpr (N >= 5 && N <= 11)
-        return try_pencil<N, 1, 3, false, 1, false, 1, true, true>(p, g, dx, w, E, s, a);
+        return try_pencil<N, 1, 3, false, 1, true, 1, true, CGM>(p, g, dx, w, E, s, a);
     else if constexpr (N == 4)
-        return try_pencil<N, 1, 2, false, 1, false, 1, false, true>(p, g, dx, w, E, s, a);
+        return try_pencil<N, 1, 2, false, 1, false, 1, false, CGM>(p, g, dx, w, E, s, a);
+    else if constexpr (CGM == 2)  // one element per CTA (the reduction is per CTA)
+        return try_pencil<N, 1, 2, false, 1, false, 0, false, CGM>(p, g, dx, w, E, s, a);
     else
-        return try_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, true>(p, g, dx, w,
-                                                                                    E, s, a);
+        return try_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, CGM>(p, g, dx, w,
+                                                                                   E, s, a);
 }
 
 }  // namespace sem

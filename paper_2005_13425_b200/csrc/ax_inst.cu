@@ -15,10 +15,10 @@ namespace sem {
     {                                                                                         \
         return ax_n<NV>(u, g, dx, w, E, variant, s);                                          \
     }                                                                                         \
-    int ax_cg_entry_##NV(double* p, const double* r, const double* g, const double* dx,       \
-                         double* w, int64_t E, sem_cg_state* st, double* hist, cudaStream_t s) \
+    int ax_cg_entry_##NV(const double* g, const double* dx, double* w, int64_t E,             \
+                         CgpArgs a, int mode, cudaStream_t s)                                 \
     {                                                                                         \
-        return ax_cg_n<NV>(p, r, g, dx, w, E, st, hist, s);                                   \
+        return mode == 2 ? ax_cg_n<NV, 2>(g, dx, w, E, a, s) : ax_cg_n<NV, 1>(g, dx, w, E, a, s); \
     }
 
 // groups balanced by compile cost (grows steeply with n)

@@ -26,6 +26,7 @@
 // j-pencil accesses are bank-conflict free.
 #pragma once
 #include "sem_common.cuh"
+#include "reduce.cuh"
 
 namespace sem {
 
@@ -179,19 +180,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase)
 // GMODE 2: as 1, and u also arrives by bulk copies (one per k-layer, straight
 //          into the padded U stack) on its own mbarrier, so S3 starts as soon
 //          as u lands while g is still streaming.
-// CG fusion (CGP): the top of a CG iteration (sembench/cg.py:149-160:
+// CG fusion (CGM >= 1): the top of a CG iteration (sembench/cg.py:149-160:
 // exact-zero exit, beta = rtz/rtz_old, p = beta*p + r, unfused multiply-add)
 // is folded into the Ax prologue: the kernel reads p_old and r, writes p_new
 // back and applies the operator to it -- one pass over p fewer per iteration.
+// CGM == 2 (single-GPU solver) also folds in
+//  * the PREVIOUS iteration's x += alpha p (cg.py:171), deferred so it reads
+//    the p_old this prologue loads anyway (same operands, same rounding);
+//  * <p, A p>_c (cg.py:163) as the LOCAL sum over element points of
+//    p * (A_local p): p is continuous and masked, so
+//    sum_c p . mask(dssum(w)) / mult == sum_local p . w exactly in real
+//    arithmetic (rounding-level difference, element energies >= 0 so no
+//    cancellation), and alpha = rtz / pap is settled by the last CTA --
+//    the assembly pass no longer re-reads p.
 struct CgpArgs {
     double* p;            // p (read old, write new)
     const double* r;
     sem_cg_state* st;
     double* history;
+    double* x;            // CGM == 2: x (read, write)
+    double* partials;     // CGM == 2: one double per CTA
+    unsigned* counter;    // CGM == 2: arrival counter (zero between launches)
 };
 
 template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false,
-          int GMODE = 0, bool FOLD = false, bool CGP = false>
+          int GMODE = 0, bool FOLD = false, int CGM = 0>
 __global__ void __launch_bounds__(THREADS, MINB)
 ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                  double* __restrict__ w, int64_t num_elements, const DParamP<N> D,
@@ -228,8 +241,9 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     // otherwise one batch per CTA (D constants are not loop-invariant, so
     // the compiler keeps them in uniform registers only around their use).
 
-    double beta = 0.0;
-    if constexpr (CGP) {
+    double beta = 0.0, alpha_prev = 0.0;
+    bool xpend = false;
+    if constexpr (CGM != 0) {
         static_assert(!PERSIST && GMODE != 2, "CG fusion: one batch per CTA, u via registers");
         sem_cg_state* st = cgp.st;
         if (st->stop) return;                       // uniform over the grid
@@ -244,18 +258,49 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             return;
         }
         beta = (it == 1) ? 0.0 : rtz / st->rtz_old;
+        if constexpr (CGM == 2) {
+            xpend = st->x_pending != 0;
+            alpha_prev = st->alpha;
+        }
         if (blockIdx.x == 0 && tid == 0) st->beta = beta;
     }
+    double pap_acc = 0.0;
     double ucol[N];
     auto load_ucol = [&](int64_t b) {
         const int64_t e = b * SLOTS + slot;
         const bool ok = lane_ok && b < nbatches && e < num_elements;
-        if constexpr (CGP) {
-            double* pp = cgp.p + (ok ? e : 0) * NNN + kp_j * N + kp_i;
-            const double* rp = cgp.r + (ok ? e : 0) * NNN + kp_j * N + kp_i;
+        if constexpr (CGM != 0) {
+            const int64_t off = (ok ? e : 0) * NNN + kp_j * N + kp_i;
+            double* pp = cgp.p + off;
+            const double* rp = cgp.r + off;
+            if (CGM == 2 && xpend && ok) {  // x += alpha_prev * p_old (cg.py:171)
+                // every load issued before any store (p, x, r may alias as far
+                // as the compiler knows)
+                double* xp = cgp.x + off;
+                double xv[N], rv[N];
 #pragma unroll
-            for (int k = 0; k < N; ++k)
-                ucol[k] = ok ? add_rn(mul_rn(beta, pp[k * NN]), __ldg(rp + k * NN)) : 0.0;
+                for (int k = 0; k < N; ++k) {
+                    ucol[k] = pp[k * NN];
+                    xv[k] = xp[k * NN];
+                    rv[k] = __ldg(rp + k * NN);
+                }
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    xv[k] = add_rn(xv[k], mul_rn(alpha_prev, ucol[k]));
+                    ucol[k] = add_rn(mul_rn(beta, ucol[k]), rv[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < N; ++k) xp[k * NN] = xv[k];
+            } else {
+                double pv[N], rv[N];
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    pv[k] = ok ? pp[k * NN] : 0.0;
+                    rv[k] = ok ? __ldg(rp + k * NN) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < N; ++k) ucol[k] = ok ? add_rn(mul_rn(beta, pv[k]), rv[k]) : 0.0;
+            }
             if (ok) {
 #pragma unroll
                 for (int k = 0; k < N; ++k) pp[k * NN] = ucol[k];
@@ -311,6 +356,12 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         if (L2PF && pf_elems > 0 && lane_ok && p == 0 && e + pf_elems < num_elements) {
             const int64_t en = e + pf_elems;
             prefetch_l2_bulk(u, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);
+            if constexpr (CGM != 0) {
+                prefetch_l2_bulk(cgp.r, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);
+                if (CGM == 2)
+                    prefetch_l2_bulk(cgp.x, en * NNN * 8, (en + 1) * NNN * 8,
+                                     num_elements * NNN * 8);
+            }
             prefetch_l2_bulk(g, en * 6 * NNN * 8, (en + 1) * 6 * NNN * 8,
                              num_elements * 6 * NNN * 8);
         }
@@ -456,11 +507,43 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             for (int k = 0; k < N; ++k) {
                 const double v = (A[k * LSA + p] + B[k * LSB + p]) + Wt[k];
                 __stcs(we + k * NN, v);
+                if constexpr (CGM == 2) pap_acc = fma(U[k * LSU + p], v, pap_acc);  // U = p_new
             }
         }
         // (no barrier needed: the next S3 writes only U, last read before the
         //  second barrier of this iteration; A/B are next written after S3's
         //  barrier)
+    }
+    if constexpr (CGM == 2) {
+        // <p, A p>: CTA partial -> partials[blockIdx.x]; the last CTA to
+        // arrive sums them in a fixed order and settles alpha (cg.py:163-170)
+        __shared__ double red_sh[THREADS / 32];
+        __shared__ bool red_last;
+        const double tot = block_sum<THREADS>(pap_acc, red_sh);
+        if (tid == 0) {
+            cgp.partials[blockIdx.x] = tot;
+            __threadfence();
+            red_last = atomicAdd(cgp.counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (!red_last) return;
+        __threadfence();
+        double v = 0.0;
+#pragma unroll 8
+        for (int b = tid; b < (int)gridDim.x; b += THREADS) v += __ldcg(cgp.partials + b);
+        const double pap = block_sum<THREADS>(v, red_sh);
+        if (tid == 0) {
+            sem_cg_state* st = cgp.st;
+            *cgp.counter = 0u;
+            st->x_pending = 0;  // every CTA applied it above
+            st->pap = pap;
+            if (pap <= 0.0) {   // cg.py:164-169 breakdown
+                st->stop = 2;
+                st->breakdown_it = st->it + 1;
+            } else {
+                st->alpha = st->rtz / pap;
+            }
+        }
     }
 }
 

@@ -7,11 +7,23 @@
 //   the weight 1/multiplicity is recomputed from the lattice, so the three
 //   weighted dots of an iteration read 2 streams instead of 3.
 // * The CG driver keeps rtz / pap / alpha / beta in a device-side
-//   sem_cg_state: an iteration is four launches (p-update, Ax, dssum+mask
-//   fused with <p,w>_c, x/r-update fused with <r,r>_c) with no host
-//   synchronisation; early exits (rtz == 0, tolerance, breakdown) set a
-//   device stop flag that turns the remaining queued launches into no-ops.
+//   sem_cg_state and never synchronises the host; early exits (rtz == 0,
+//   tolerance, breakdown) set a device stop flag that turns the remaining
+//   queued launches into no-ops.  Single GPU (sem_cg_run): TWO launches per
+//   iteration --
+//     1. Ax with the iteration head fused in (ax_pencil.cuh, CGM = 2):
+//        x += alpha_prev p_old (deferred from the previous iteration),
+//        p = beta p + r, w = A_local p, <p, A p> -> alpha;
+//     2. cg_update2_kernel: r += (-alpha) mask(dssum(w)) with the ordered
+//        dssum gathered per row, and <r, r>_c -> rnorm, beta's numerator;
+//   and sem_cg_finalize applies the last pending x update.  120 B per point
+//   per iteration (Ax 96: p, x read+write, r, g, w; update 24: w, r r+w)
+//   against the 240 B of the paper's model.  The multi-GPU slab solver keeps
+//   the three-launch form (p update in the Ax prologue, assemble + <p,w>_c,
+//   update + <r,r>_c) whose reductions are exchanged between ranks.
 #include <math.h>
+
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -19,13 +31,14 @@
 #include "reduce.cuh"
 #include "flat.cuh"
 #include "rows.cuh"
+#include "ax_pencil.cuh"
 
 namespace sem {
 
 int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
                 int n, int variant, cudaStream_t stream);
-int ax_cg_dispatch(double* p, const double* r, const double* g, const double* dx, double* w,
-                   int64_t E, int n, sem_cg_state* st, double* hist, cudaStream_t stream);
+int ax_cg_dispatch(const double* g, const double* dx, double* w, int64_t E, int n, CgpArgs a,
+                   int mode, cudaStream_t stream);
 
 constexpr int kVecThreads = 256;
 
@@ -118,6 +131,7 @@ __device__ __forceinline__ void fin_init(sem_cg_state* st, double rtz)
     st->iterations_run = 0;
     st->stop = 0;
     st->breakdown_it = 0;
+    st->x_pending = 0;
 }
 
 __device__ __forceinline__ void fin_pap(sem_cg_state* st, double pap)
@@ -297,6 +311,22 @@ static unsigned row_grid(int64_t E)
     return (unsigned)(blocks < kReduceBlocks ? (blocks > 0 ? blocks : 1) : kReduceBlocks);
 }
 
+// update2 grid: about four rows per thread, between kReduceBlocks and
+// kReduceBlocksMax blocks (tools/cg_tune.sh: at E = 4096 1184 blocks beat
+// one row per thread, at E = 32768 4736 blocks beat 1184 by 17%).  A
+// function of E and n only, so the reduction tree is fixed.
+template <int N>
+static unsigned upd_grid(int64_t E)
+{
+    static const int cap = getenv("SEM_CG_UPD_BLOCKS") ? atoi(getenv("SEM_CG_UPD_BLOCKS")) : 0;
+    const int64_t rows = E * N * N;
+    int64_t blocks = (rows + 4 * kRowThreads - 1) / (4 * kRowThreads);
+    blocks = std::max<int64_t>(blocks, std::min<int64_t>(kReduceBlocks, (rows + kRowThreads - 1) / kRowThreads));
+    blocks = std::min<int64_t>(blocks, kReduceBlocksMax);
+    if (cap > 0 && cap <= kReduceBlocksMax) blocks = std::min<int64_t>(blocks, cap);
+    return (unsigned)(blocks > 0 ? blocks : 1);
+}
+
 template <int N>
 static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_state* st,
                      int64_t E, Box bx, ReduceScratch* rs, int max_it, double tol,
@@ -308,6 +338,54 @@ static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_st
     return 0;
 }
 
+// Single-GPU iteration tail (cg.py:170-186 minus the x update, which the
+// next Ax prologue applies): r += (-alpha) mask(dssum(w)), with the ordered
+// row gather of rows.cuh (bit-identical to the assemble kernel's w2), and
+// <r, r>_c -> history, tolerance flag, beta's numerator.
+template <int N>
+__global__ void __launch_bounds__(kRowThreads)
+cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, Box bx,
+                  sem_cg_state* st, double* history, ReduceScratch* rs)
+{
+    constexpr int NN = N * N, NNN = N * N * N;
+    if (st->stop) return;
+    const double nalpha = -st->alpha;
+    double acc = 0.0;
+    for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < E * NN;
+         row += (int64_t)gridDim.x * kRowThreads) {
+        const Row<N> rw = make_row<N>(row, bx);
+        const int64_t base = rw.e * NNN + rw.jk * N;
+        double v[N], rv[N];
+        dssum_row<N>(w, rw, bx, nullptr, nullptr, v);
+        load_row_rw<N>(r + base, rv);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            rv[i] = add_rn(rv[i], mul_rn(nalpha, mul_rn(v[i], row_mask<N>(rw, i))));
+            acc += mul_rn(mul_rn(rv[i], rv[i]), row_inv_mult<N>(rw, i));
+        }
+        store_row<N>(r + base, rv);
+    }
+    const double vals[1] = {acc};
+    reduce_publish_and_finish<1, kRowThreads>(vals, rs, [&](const double (&t)[1]) {
+        fin_rr(st, t[0], history);
+        st->x_pending = 1;  // x += alpha p of this iteration is owed
+    });
+}
+
+// The owed x += alpha p of the last iteration (every exit except breakdown).
+__global__ void __launch_bounds__(kVecThreads)
+cg_finalize_kernel(double* __restrict__ x, const double* __restrict__ p, int64_t m,
+                   const sem_cg_state* st)
+{
+    if (!st->x_pending || st->stop == 2) return;
+    const double alpha = st->alpha;
+    const int64_t stride = (int64_t)gridDim.x * kVecThreads;
+    for (int64_t q = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; q < m; q += stride)
+        x[q] = add_rn(x[q], mul_rn(alpha, __ldg(p + q)));
+}
+
+__global__ void cg_clear_pending_kernel(sem_cg_state* st) { st->x_pending = 0; }
+
 template <int N>
 static int cg_run_n(const double* g, const double* dx, double* x, double* r, double* p,
                     double* w, double* w2, sem_cg_state* st, double* history, int iters,
@@ -317,18 +395,16 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
     // marks (optional, 3*iters+1 events): recorded before each iteration's
     // Ax, assemble and update launches and after the last one
     auto mark = [&](int q) { return marks ? cudaEventRecord(marks[q], s) : cudaSuccess; };
+    // w2 (the second half of the w scratch) holds the Ax kernel's per-CTA
+    // <p, A p> partials (one per element at most)
+    const CgpArgs a{p, r, st, history, x, w2, &rs->counter};
     for (int it = 0; it < iters; ++it) {
         if (cudaError_t e = mark(3 * it)) return fail_cuda(e, "sem_cg_run: event");
-        // p = beta p + r fused into the Ax prologue (ax_pencil.cuh, CGP)
-        if (int rc = ax_cg_dispatch(p, r, g, dx, w, E, N, st, history, s)) return rc;
+        if (int rc = ax_cg_dispatch(g, dx, w, E, N, a, 2, s)) return rc;
         if (cudaError_t e = mark(3 * it + 1)) return fail_cuda(e, "sem_cg_run: event");
-        cg_assemble_kernel<N, false><<<row_grid<N>(E), kRowThreads, 0, s>>>(w, w2, p, E, bx, st,
-                                                                             rs, nullptr, nullptr);
-        SEM_CHECK_LAUNCH("cg_assemble_kernel");
+        cg_update2_kernel<N><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, bx, st, history, rs);
+        SEM_CHECK_LAUNCH("cg_update2_kernel");
         if (cudaError_t e = mark(3 * it + 2)) return fail_cuda(e, "sem_cg_run: event");
-        cg_update_kernel<N, false><<<red_grid<N>(E), PairCfg<N>::THREADS, 0, s>>>(x, r, p, w2, E, make_box_flat(bx),
-                                                                           st, history, rs);
-        SEM_CHECK_LAUNCH("cg_update_kernel");
     }
     if (cudaError_t e = mark(3 * iters)) return fail_cuda(e, "sem_cg_run: event");
     return 0;
@@ -441,10 +517,28 @@ extern "C" int sem_cg_run(const double* g, const double* dx, const double* dxt, 
                                         iterations, E, bx, rs, s));
 }
 
+extern "C" int sem_cg_finalize(double* x, const double* p, sem_cg_state* state,
+                               int64_t num_points, sem_stream_t stream)
+{
+    if (!x || !p || !state || num_points < 0) {
+        set_error("sem_cg_finalize: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    cg_finalize_kernel<<<vec_grid(num_points > 0 ? num_points : 1), kVecThreads, 0, s>>>(
+        x, p, num_points, state);
+    SEM_CHECK_LAUNCH("cg_finalize_kernel");
+    cg_clear_pending_kernel<<<1, 1, 0, s>>>(state);
+    SEM_CHECK_LAUNCH("cg_clear_pending_kernel");
+    return 0;
+}
+
 // Instrumented form of sem_cg_run: the same launches, eagerly, with CUDA
 // events between them; synchronises and adds each phase's device time (ms)
-// to phase_ms[0] (Ax incl. the fused p update), [1] (assemble: dssum + mask
-// + <p,w>), [2] (x/r updates + <r,r>).  Measurement only (harness.py).
+// to phase_ms[0] (Ax with the fused iteration head and <p, A p>), [1] (r
+// update with the fused dssum + mask, <r,r>), [2] (unused, 0).  Measurement
+// only (harness.py).
 extern "C" int sem_cg_run_phases(const double* g, const double* dx, const double* dxt, double* x,
                                  double* r, double* p, double* w, sem_cg_state* state,
                                  double* history, int32_t iterations, int32_t ex, int32_t ey,
@@ -573,7 +667,8 @@ extern "C" int sem_cg_ax(double* p, const double* r, const double* g, const doub
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (int rc = bind_stream_device(s)) return rc;
-    return ax_cg_dispatch(p, r, g, dx, w, num_elements, n, state, history, s);
+    const CgpArgs a{p, r, state, history, nullptr, nullptr, nullptr};
+    return ax_cg_dispatch(g, dx, w, num_elements, n, a, 1, s);
 }
 
 extern "C" int sem_cg_assemble_slab(const double* w, double* w2, const double* p,

@@ -13,12 +13,13 @@
 namespace sem {
 
 constexpr int kReduceBlocks = 1184;  // 8 x 148; a constant so the tree is fixed
+constexpr int kReduceBlocksMax = 4 * kReduceBlocks;  // capacity of the partial slots
 constexpr int kReduceThreads = 256;
 constexpr int kMaxReductions = 4;    // independent accumulators per kernel
 
-// scratch layout: double partials[kMaxReductions][kReduceBlocks]; uint32 counter
+// scratch layout: double partials[kMaxReductions][kReduceBlocksMax]; uint32 counter
 struct ReduceScratch {
-    double partials[kMaxReductions][kReduceBlocks];
+    double partials[kMaxReductions][kReduceBlocksMax];
     unsigned int counter;
     unsigned int pad[15];
 };
