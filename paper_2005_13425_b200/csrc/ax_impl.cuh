@@ -372,7 +372,7 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 // prefetch depth, persistent, L2 bulk prefetch>.
 // Default tuning point per n (tools/ax_sweep.py on B200, E=4096; see
 // profiles/r01_ax_sweep.txt, CUDA-graph timed): index = n, value = variant id.
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 5, 8, 7, 17, 3};
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 24, 46, 42, 46, 43};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
@@ -406,6 +406,12 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
         // + bulk L2 prefetch of the element a resident wave ahead
         case 40: return try_pencil<N, 1, 3, false, 1, true, 1, true>(u, g, dx, w, E, stream);
         case 41: return try_pencil<N, 1, 2, false, 1, true, 1, true>(u, g, dx, w, E, stream);
+        // large n: folded contractions with the metric register ring
+        case 42: return try_pencil<N, 1, 2, false, 1, false, 0, true>(u, g, dx, w, E, stream);
+        case 43: return try_pencil<N, 1, 2, false, 2, false, 0, true>(u, g, dx, w, E, stream);
+        case 44: return try_pencil<N, 1, 2, false, 1, true, 0, true>(u, g, dx, w, E, stream);
+        case 45: return try_pencil<N, 1, 3, false, 1, false, 0, true>(u, g, dx, w, E, stream);
+        case 46: return try_pencil<N, 1, 1, false, 2, false, 0, true>(u, g, dx, w, E, stream);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
