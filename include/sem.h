@@ -199,25 +199,29 @@ int sem_glsc3_slab(const double *a, const double *b, int32_t ex, int32_t ey, int
  * state->local_sum; after gathering all ranks' partials (rank order) into
  * `gathered`, sem_cg_finish(phase) combines them in rank order and performs
  * the phase's scalar step (0: rtz after init, 1: pap -> alpha / breakdown,
- * 2: <r,r> -> history, rtz, tolerance). */
+ * 2: <r,r> -> history, rtz, tolerance, x update owed). */
 int sem_cg_init_slab(const double *f, double *x, double *r, double *p, sem_cg_state *state,
                      double *history, int32_t max_iterations, double tolerance, int32_t ex,
                      int32_t ey, int32_t ez, int32_t n, int32_t gz0, int32_t ez_global,
                      void *scratch, sem_stream_t stream);
-int sem_cg_p(double *p, const double *r, int64_t m, sem_cg_state *state, double *history,
-             sem_stream_t stream);
-/* Iteration head fused with the operator: exact-zero exit / beta / p = beta*p + r
- * (cg.py:149-160) in the Ax prologue, then w = A_local p (one launch). */
-int sem_cg_ax(double *p, const double *r, const double *g, const double *dx, const double *dxt,
-              double *w, int64_t num_elements, int32_t n, sem_cg_state *state,
-              double *history, sem_stream_t stream);
-int sem_cg_assemble_slab(const double *w, double *w2, const double *p,
-                         const double *bottom_totals, const double *top_totals,
-                         sem_cg_state *state, int32_t ex, int32_t ey, int32_t ez, int32_t n,
-                         int32_t gz0, int32_t ez_global, void *scratch, sem_stream_t stream);
-int sem_cg_update_slab(double *x, double *r, const double *p, const double *w2,
-                       sem_cg_state *state, int32_t ex, int32_t ey, int32_t ez, int32_t n,
-                       int32_t gz0, int32_t ez_global, void *scratch, sem_stream_t stream);
+/* The single-GPU iteration's two kernels on a slab (each rank, every
+ * iteration): sem_cg_ax_slab on element ranges of the slab (edge layers
+ * first, then the interior overlapping the halo exchange) = exact-zero exit,
+ * beta, x += alpha_prev p_old (deferred), p = beta*p + r, w = A_local p and
+ * this range's sum of p*(A_local p) added to (accumulate != 0) or stored in
+ * state->local_sum -- gather + sem_cg_finish(phase 1) then settles alpha.
+ * `partials` holds one double per element of the range (device scratch).
+ * sem_cg_update_slab = r += (-alpha) mask(dssum(w)) with the interface faces
+ * from the halo totals, and this rank's <r,r>_c partial in local_sum
+ * (phase 2).  sem_cg_finalize applies the last owed x update. */
+int sem_cg_ax_slab(double *p, const double *r, double *x, const double *g, const double *dx,
+                   const double *dxt, double *w, int64_t num_elements, int32_t n,
+                   sem_cg_state *state, double *history, double *partials, void *scratch,
+                   int32_t accumulate, sem_stream_t stream);
+int sem_cg_update_slab(const double *w, double *r, const double *bottom_totals,
+                       const double *top_totals, sem_cg_state *state, int32_t ex, int32_t ey,
+                       int32_t ez, int32_t n, int32_t gz0, int32_t ez_global, void *scratch,
+                       sem_stream_t stream);
 int sem_cg_finish(sem_cg_state *state, const double *gathered, int32_t nranks, int32_t phase,
                   double *history, sem_stream_t stream);
 

@@ -82,10 +82,8 @@ SIGNATURES = {
                                       _vp]),
     "sem_cg_init_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _f64, _i32, _i32,
                                         _i32, _i32, _i32, _i32, _vp, _vp]),
-    "sem_cg_p": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
-    "sem_cg_ax": (ctypes.c_int, [_vp, _vp, _vp, _dp, _dp, _vp, _i64, _i32, _vp, _vp, _vp]),
-    "sem_cg_assemble_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,
-                                            _i32, _i32, _i32, _vp, _vp]),
+    "sem_cg_ax_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _dp, _dp, _vp, _i64, _i32, _vp, _vp,
+                                      _vp, _vp, _i32, _vp]),
     "sem_cg_update_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                                           _i32, _vp, _vp]),
     "sem_cg_finish": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),

@@ -17,8 +17,8 @@ SEM_AX_DECLARE(7) SEM_AX_DECLARE(8) SEM_AX_DECLARE(9) SEM_AX_DECLARE(10) SEM_AX_
 SEM_AX_DECLARE(12) SEM_AX_DECLARE(13) SEM_AX_DECLARE(14) SEM_AX_DECLARE(15) SEM_AX_DECLARE(16)
 #undef SEM_AX_DECLARE
 
-// mode 1: p-update prologue only (multi-GPU slab solver); mode 2: also the
-// deferred x update and <p, A p> -> alpha (single-GPU solver)
+// mode 2: single-GPU solver (<p, A p> -> alpha in the last CTA); mode 3:
+// z-slab rank (<p, A p> partial -> state->local_sum)
 int ax_cg_dispatch(const double* g, const double* dx, double* w, int64_t E, int n, CgpArgs a,
                    int mode, cudaStream_t stream)
 {

@@ -437,9 +437,9 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
 
 // CG iteration head fused with Ax (p = beta p + r; w = A_local p): the tuned
 // configuration of each n with the metric staged by TMA and u through
-// registers (the p update happens while the column is loaded).  CGM = 1:
-// multi-GPU slab solver; CGM = 2: single-GPU solver (x update and <p,Ap>
-// fused too, see ax_pencil.cuh).
+// registers (the p update happens while the column is loaded), x update and
+// <p, A p> fused too (ax_pencil.cuh).  CGM = 2: single-GPU solver; CGM = 3:
+// z-slab rank of the multi-GPU solver.
 template <int N, int CGM>
 static int ax_cg_n(const double* g, const double* dx, double* w, int64_t E, CgpArgs a,
                    cudaStream_t s)
@@ -467,11 +467,8 @@ static int ax_cg_n(const double* g, const double* dx, double* w, int64_t E, CgpA
         return try_pencil<N, 1, 3, false, 1, true, 1, true, CGM>(p, g, dx, w, E, s, a);
     else if constexpr (N == 4)
         return try_pencil<N, 1, 2, false, 1, false, 1, false, CGM>(p, g, dx, w, E, s, a);
-    else if constexpr (CGM == 2)  // one element per CTA (the reduction is per CTA)
-        return try_pencil<N, 1, 2, false, 1, false, 0, false, CGM>(p, g, dx, w, E, s, a);
     else
-        return try_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, CGM>(p, g, dx, w,
-                                                                                   E, s, a);
+        return try_pencil<N, 1, 2, false, 1, false, 0, false, CGM>(p, g, dx, w, E, s, a);
 }
 
 }  // namespace sem

@@ -18,7 +18,7 @@ namespace sem {
     int ax_cg_entry_##NV(const double* g, const double* dx, double* w, int64_t E,             \
                          CgpArgs a, int mode, cudaStream_t s)                                 \
     {                                                                                         \
-        return mode == 2 ? ax_cg_n<NV, 2>(g, dx, w, E, a, s) : ax_cg_n<NV, 1>(g, dx, w, E, a, s); \
+        return mode == 3 ? ax_cg_n<NV, 3>(g, dx, w, E, a, s) : ax_cg_n<NV, 2>(g, dx, w, E, a, s); \
     }
 
 // groups balanced by compile cost (grows steeply with n)

@@ -180,27 +180,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase)
 // GMODE 2: as 1, and u also arrives by bulk copies (one per k-layer, straight
 //          into the padded U stack) on its own mbarrier, so S3 starts as soon
 //          as u lands while g is still streaming.
-// CG fusion (CGM >= 1): the top of a CG iteration (sembench/cg.py:149-160:
+// CG fusion (CGM >= 2): the top of a CG iteration (sembench/cg.py:149-160:
 // exact-zero exit, beta = rtz/rtz_old, p = beta*p + r, unfused multiply-add)
 // is folded into the Ax prologue: the kernel reads p_old and r, writes p_new
 // back and applies the operator to it -- one pass over p fewer per iteration.
-// CGM == 2 (single-GPU solver) also folds in
+// It also folds in
 //  * the PREVIOUS iteration's x += alpha p (cg.py:171), deferred so it reads
 //    the p_old this prologue loads anyway (same operands, same rounding);
 //  * <p, A p>_c (cg.py:163) as the LOCAL sum over element points of
 //    p * (A_local p): p is continuous and masked, so
 //    sum_c p . mask(dssum(w)) / mult == sum_local p . w exactly in real
 //    arithmetic (rounding-level difference, element energies >= 0 so no
-//    cancellation), and alpha = rtz / pap is settled by the last CTA --
-//    the assembly pass no longer re-reads p.
+//    cancellation).  CGM == 2 (single GPU): the last CTA settles
+//    alpha = rtz / pap.  CGM == 3 (z-slab rank): the last CTA adds this
+//    launch's sum to state->local_sum (reset by the first launch of an
+//    iteration), which the ranks then combine (dist.py).
 struct CgpArgs {
     double* p;            // p (read old, write new)
     const double* r;
     sem_cg_state* st;
     double* history;
-    double* x;            // CGM == 2: x (read, write)
-    double* partials;     // CGM == 2: one double per CTA
-    unsigned* counter;    // CGM == 2: arrival counter (zero between launches)
+    double* x;            // x (read, write)
+    double* partials;     // one double per CTA
+    unsigned* counter;    // arrival counter (zero between launches)
+    int accumulate;       // CGM == 3: add to (1) or reset (0) state->local_sum
 };
 
 template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false,
@@ -258,10 +261,8 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             return;
         }
         beta = (it == 1) ? 0.0 : rtz / st->rtz_old;
-        if constexpr (CGM == 2) {
-            xpend = st->x_pending != 0;
-            alpha_prev = st->alpha;
-        }
+        xpend = st->x_pending != 0;
+        alpha_prev = st->alpha;
         if (blockIdx.x == 0 && tid == 0) st->beta = beta;
     }
     double pap_acc = 0.0;
@@ -273,7 +274,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             const int64_t off = (ok ? e : 0) * NNN + kp_j * N + kp_i;
             double* pp = cgp.p + off;
             const double* rp = cgp.r + off;
-            if (CGM == 2 && xpend && ok) {  // x += alpha_prev * p_old (cg.py:171)
+            if (xpend && ok) {  // x += alpha_prev * p_old (cg.py:171)
                 // every load issued before any store (p, x, r may alias as far
                 // as the compiler knows)
                 double* xp = cgp.x + off;
@@ -358,9 +359,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             prefetch_l2_bulk(u, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);
             if constexpr (CGM != 0) {
                 prefetch_l2_bulk(cgp.r, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);
-                if (CGM == 2)
-                    prefetch_l2_bulk(cgp.x, en * NNN * 8, (en + 1) * NNN * 8,
-                                     num_elements * NNN * 8);
+                prefetch_l2_bulk(cgp.x, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);
             }
             prefetch_l2_bulk(g, en * 6 * NNN * 8, (en + 1) * 6 * NNN * 8,
                              num_elements * 6 * NNN * 8);
@@ -507,14 +506,14 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             for (int k = 0; k < N; ++k) {
                 const double v = (A[k * LSA + p] + B[k * LSB + p]) + Wt[k];
                 __stcs(we + k * NN, v);
-                if constexpr (CGM == 2) pap_acc = fma(U[k * LSU + p], v, pap_acc);  // U = p_new
+                if constexpr (CGM != 0) pap_acc = fma(U[k * LSU + p], v, pap_acc);  // U = p_new
             }
         }
         // (no barrier needed: the next S3 writes only U, last read before the
         //  second barrier of this iteration; A/B are next written after S3's
         //  barrier)
     }
-    if constexpr (CGM == 2) {
+    if constexpr (CGM != 0) {
         // <p, A p>: CTA partial -> partials[blockIdx.x]; the last CTA to
         // arrive sums them in a fixed order and settles alpha (cg.py:163-170)
         __shared__ double red_sh[THREADS / 32];
@@ -535,6 +534,10 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         if (tid == 0) {
             sem_cg_state* st = cgp.st;
             *cgp.counter = 0u;
+            if constexpr (CGM == 3) {  // this rank's partial; combined across ranks later
+                st->local_sum = (cgp.accumulate ? st->local_sum : 0.0) + pap;
+                return;
+            }
             st->x_pending = 0;  // every CTA applied it above
             st->pap = pap;
             if (pap <= 0.0) {   // cg.py:164-169 breakdown

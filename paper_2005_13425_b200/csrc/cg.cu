@@ -18,9 +18,9 @@
 //        dssum gathered per row, and <r, r>_c -> rnorm, beta's numerator;
 //   and sem_cg_finalize applies the last pending x update.  120 B per point
 //   per iteration (Ax 96: p, x read+write, r, g, w; update 24: w, r r+w)
-//   against the 240 B of the paper's model.  The multi-GPU slab solver keeps
-//   the three-launch form (p update in the Ax prologue, assemble + <p,w>_c,
-//   update + <r,r>_c) whose reductions are exchanged between ranks.
+//   against the 240 B of the paper's model.  The multi-GPU slab solver runs
+//   the same two kernels per rank (sem_cg_ax_slab, sem_cg_update_slab), each
+//   leaving a partial sum that the ranks combine (sem_cg_finish).
 #include <math.h>
 
 #include <stdlib.h>
@@ -137,6 +137,7 @@ __device__ __forceinline__ void fin_init(sem_cg_state* st, double rtz)
 __device__ __forceinline__ void fin_pap(sem_cg_state* st, double pap)
 {
     st->pap = pap;
+    st->x_pending = 0;  // the Ax prologues of this iteration applied it
     if (pap <= 0.0) {  // cg.py:164-169 breakdown
         st->stop = 2;
         st->breakdown_it = st->it + 1;
@@ -154,6 +155,7 @@ __device__ __forceinline__ void fin_rr(sem_cg_state* st, double rtr, double* his
     st->rtz_old = st->rtz;
     st->rtz = rtr;  // equals <r,r>_c at the top of the next iteration
     st->it = it;
+    st->x_pending = 1;  // x += alpha p of this iteration: next Ax prologue / finalize
     if (st->tolerance > 0.0 && rnorm < st->tolerance) st->stop = 3;
 }
 
@@ -203,97 +205,6 @@ cg_init_kernel(const double* __restrict__ f, double* __restrict__ x, double* __r
     });
 }
 
-// Top of an iteration (cg.py:149-160): exact-zero exit, beta, p = beta p + r.
-__global__ void __launch_bounds__(kVecThreads)
-cg_p_kernel(double* __restrict__ p, const double* __restrict__ r, int64_t m, sem_cg_state* st,
-            double* history)
-{
-    if (st->stop) return;
-    const int it = st->it + 1;
-    const double rtz = st->rtz;
-    if (rtz == 0.0) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            history[it - 1] = 0.0;
-            st->iterations_run = it;
-            st->stop = 1;
-        }
-        return;
-    }
-    const double beta = (it == 1) ? 0.0 : rtz / st->rtz_old;
-    const int64_t stride = (int64_t)gridDim.x * kVecThreads;
-    for (int64_t q = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; q < m; q += stride)
-        p[q] = add_rn(mul_rn(beta, p[q]), __ldg(r + q));
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->beta = beta;
-}
-
-// w2 = mask(dssum(w)) and <p, w2>_c (assembly.py:113-129 + cg.py:163-170).
-template <int N, bool DIST>
-__global__ void __launch_bounds__(kRowThreads)
-cg_assemble_kernel(const double* __restrict__ w, double* __restrict__ w2,
-                   const double* __restrict__ p, int64_t E, Box bx, sem_cg_state* st,
-                   ReduceScratch* rs, const double* __restrict__ bot,
-                   const double* __restrict__ top)
-{
-    constexpr int NN = N * N, NNN = N * N * N;
-    if (st->stop) return;
-    double acc = 0.0;
-    for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < E * NN;
-         row += (int64_t)gridDim.x * kRowThreads) {
-        const Row<N> rw = make_row<N>(row, bx);
-        const int64_t base = rw.e * NNN + rw.jk * N;
-        double v[N], pv[N];
-        dssum_row<N>(w, rw, bx, DIST ? bot : nullptr, DIST ? top : nullptr, v);
-        load_row<N>(p + base, pv);
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            v[i] = mul_rn(v[i], row_mask<N>(rw, i));
-            acc += mul_rn(mul_rn(pv[i], v[i]), row_inv_mult<N>(rw, i));
-        }
-        store_row<N>(w2 + base, v);
-    }
-    const double vals[1] = {acc};
-    reduce_publish_and_finish<1, kRowThreads>(vals, rs, [&](const double (&t)[1]) {
-        if (DIST) st->local_sum = t[0];
-        else fin_pap(st, t[0]);
-    });
-}
-
-// x += alpha p ; r += (-alpha) w2 ; rnorm = sqrt(<r,r>_c)  (cg.py:170-186).
-template <int N, bool DIST>
-__global__ void __launch_bounds__(PairCfg<N>::THREADS)
-cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                 const double* __restrict__ w2, int64_t E, BoxFlat bf, sem_cg_state* st,
-                 double* history, ReduceScratch* rs)
-{
-    if (st->stop) return;
-    const double alpha = st->alpha, nalpha = -alpha;
-    double acc = 0.0;
-    SEM_PAIR_LOOP(E) {
-        const int64_t q0 = u_ * NP;
-        ElemCoord c;
-        int i, j, k;
-        pair_point<N>(q0, bf, c, i, j, k);
-        double xv[NP], rv[NP], pv[NP], wv[NP];
-        ld_pair_rw<N>(x + q0, xv);
-        ld_pair_rw<N>(r + q0, rv);
-        ld_pair<N>(p + q0, pv);
-        ld_pair<N>(w2 + q0, wv);
-#pragma unroll
-        for (int h = 0; h < NP; ++h) {
-            xv[h] = add_rn(xv[h], mul_rn(alpha, pv[h]));
-            rv[h] = add_rn(rv[h], mul_rn(nalpha, wv[h]));
-            acc += mul_rn(mul_rn(rv[h], rv[h]), inv_mult_of<N>(c, i + h, j, k, bf.b));
-        }
-        st_pair<N>(x + q0, xv);
-        st_pair<N>(r + q0, rv);
-    }
-    const double vals[1] = {acc};
-    reduce_publish_and_finish<1, PairCfg<N>::THREADS>(vals, rs, [&](const double (&t)[1]) {
-        if (DIST) st->local_sum = t[0];
-        else fin_rr(st, t[0], history);
-    });
-}
-
 // fixed-size grid for the row reductions (a function of E and n only, so
 // the reduction tree -- and every result -- is reproducible)
 // fixed grids for the reductions (functions of E and n only, so the
@@ -338,14 +249,16 @@ static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_st
     return 0;
 }
 
-// Single-GPU iteration tail (cg.py:170-186 minus the x update, which the
-// next Ax prologue applies): r += (-alpha) mask(dssum(w)), with the ordered
-// row gather of rows.cuh (bit-identical to the assemble kernel's w2), and
-// <r, r>_c -> history, tolerance flag, beta's numerator.
-template <int N>
+// Iteration tail (cg.py:170-186 minus the x update, which the next Ax
+// prologue applies): r += (-alpha) mask(dssum(w)), with the ordered row
+// gather of rows.cuh (faces shared with another rank from the halo planes),
+// and <r, r>_c -> history, tolerance flag, beta's numerator (DIST: this
+// rank's partial -> state->local_sum, combined by sem_cg_finish).
+template <int N, bool DIST>
 __global__ void __launch_bounds__(kRowThreads)
 cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, Box bx,
-                  sem_cg_state* st, double* history, ReduceScratch* rs)
+                  sem_cg_state* st, double* history, ReduceScratch* rs,
+                  const double* __restrict__ bot, const double* __restrict__ top)
 {
     constexpr int NN = N * N, NNN = N * N * N;
     if (st->stop) return;
@@ -356,7 +269,7 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         const Row<N> rw = make_row<N>(row, bx);
         const int64_t base = rw.e * NNN + rw.jk * N;
         double v[N], rv[N];
-        dssum_row<N>(w, rw, bx, nullptr, nullptr, v);
+        dssum_row<N>(w, rw, bx, DIST ? bot : nullptr, DIST ? top : nullptr, v);
         load_row_rw<N>(r + base, rv);
 #pragma unroll
         for (int i = 0; i < N; ++i) {
@@ -367,8 +280,8 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     }
     const double vals[1] = {acc};
     reduce_publish_and_finish<1, kRowThreads>(vals, rs, [&](const double (&t)[1]) {
-        fin_rr(st, t[0], history);
-        st->x_pending = 1;  // x += alpha p of this iteration is owed
+        if (DIST) st->local_sum = t[0];
+        else fin_rr(st, t[0], history);
     });
 }
 
@@ -402,7 +315,8 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
         if (cudaError_t e = mark(3 * it)) return fail_cuda(e, "sem_cg_run: event");
         if (int rc = ax_cg_dispatch(g, dx, w, E, N, a, 2, s)) return rc;
         if (cudaError_t e = mark(3 * it + 1)) return fail_cuda(e, "sem_cg_run: event");
-        cg_update2_kernel<N><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, bx, st, history, rs);
+        cg_update2_kernel<N, false><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, bx, st, history,
+                                                                          rs, nullptr, nullptr);
         SEM_CHECK_LAUNCH("cg_update2_kernel");
         if (cudaError_t e = mark(3 * it + 2)) return fail_cuda(e, "sem_cg_run: event");
     }
@@ -642,66 +556,31 @@ extern "C" int sem_cg_init_slab(const double* f, double* x, double* r, double* p
     });
 }
 
-extern "C" int sem_cg_p(double* p, const double* r, int64_t m, sem_cg_state* state,
-                        double* history, sem_stream_t stream)
+extern "C" int sem_cg_ax_slab(double* p, const double* r, double* x, const double* g,
+                              const double* dx, const double* dxt, double* w,
+                              int64_t num_elements, int32_t n, sem_cg_state* state,
+                              double* history, double* partials, void* scratch,
+                              int32_t accumulate, sem_stream_t stream)
 {
-    if (!p || !r || !state || !history || m < 0) {
-        set_error("sem_cg_p: bad arguments");
+    if (!p || !r || !x || !g || !dx || !dxt || !w || !state || !history || !partials ||
+        !scratch || num_elements < 0 || n < 2 || n > 16) {
+        set_error("sem_cg_ax_slab: bad arguments");
         return SEM_E_INVALID;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (int rc = bind_stream_device(s)) return rc;
-    cg_p_kernel<<<vec_grid(m), kVecThreads, 0, s>>>(p, r, m, state, history);
-    SEM_CHECK_LAUNCH("sem_cg_p launch");
-    return 0;
-}
-
-extern "C" int sem_cg_ax(double* p, const double* r, const double* g, const double* dx,
-                         const double* dxt, double* w, int64_t num_elements, int32_t n,
-                         sem_cg_state* state, double* history, sem_stream_t stream)
-{
-    if (!p || !r || !g || !dx || !dxt || !w || !state || !history || num_elements < 0 ||
-        n < 2 || n > 16) {
-        set_error("sem_cg_ax: bad arguments");
-        return SEM_E_INVALID;
-    }
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (int rc = bind_stream_device(s)) return rc;
-    const CgpArgs a{p, r, state, history, nullptr, nullptr, nullptr};
-    return ax_cg_dispatch(g, dx, w, num_elements, n, a, 1, s);
-}
-
-extern "C" int sem_cg_assemble_slab(const double* w, double* w2, const double* p,
-                                    const double* bottom_totals, const double* top_totals,
-                                    sem_cg_state* state, int32_t ex, int32_t ey, int32_t ez,
-                                    int32_t n, int32_t gz0, int32_t ez_global, void* scratch,
-                                    sem_stream_t stream)
-{
-    if (int rc = check_slab(ex, ey, ez, n, gz0, ez_global, "sem_cg_assemble_slab")) return rc;
-    if (!w || !w2 || !p || !state || !scratch || w == w2) {
-        set_error("sem_cg_assemble_slab: bad arguments");
-        return SEM_E_INVALID;
-    }
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (int rc = bind_stream_device(s)) return rc;
-    const Box bx = slab_box(ex, ey, ez, gz0, ez_global);
-    const int64_t E = (int64_t)ex * ey * ez;
     auto* rs = static_cast<ReduceScratch*>(scratch);
-    SEM_SWITCH_N(n, {
-        cg_assemble_kernel<NV, true><<<row_grid<NV>(E), kRowThreads, 0, s>>>(
-            w, w2, p, E, bx, state, rs, bottom_totals, top_totals);
-        SEM_CHECK_LAUNCH("sem_cg_assemble_slab launch");
-        return 0;
-    });
+    const CgpArgs a{p, r, state, history, x, partials, &rs->counter, accumulate ? 1 : 0};
+    return ax_cg_dispatch(g, dx, w, num_elements, n, a, 3, s);
 }
 
-extern "C" int sem_cg_update_slab(double* x, double* r, const double* p, const double* w2,
-                                  sem_cg_state* state, int32_t ex, int32_t ey, int32_t ez,
-                                  int32_t n, int32_t gz0, int32_t ez_global, void* scratch,
-                                  sem_stream_t stream)
+extern "C" int sem_cg_update_slab(const double* w, double* r, const double* bottom_totals,
+                                  const double* top_totals, sem_cg_state* state, int32_t ex,
+                                  int32_t ey, int32_t ez, int32_t n, int32_t gz0,
+                                  int32_t ez_global, void* scratch, sem_stream_t stream)
 {
     if (int rc = check_slab(ex, ey, ez, n, gz0, ez_global, "sem_cg_update_slab")) return rc;
-    if (!x || !r || !p || !w2 || !state || !scratch) {
+    if (!w || !r || !state || !scratch || w == r) {
         set_error("sem_cg_update_slab: bad arguments");
         return SEM_E_INVALID;
     }
@@ -711,8 +590,8 @@ extern "C" int sem_cg_update_slab(double* x, double* r, const double* p, const d
     const int64_t E = (int64_t)ex * ey * ez;
     auto* rs = static_cast<ReduceScratch*>(scratch);
     SEM_SWITCH_N(n, {
-        cg_update_kernel<NV, true><<<red_grid<NV>(E), PairCfg<NV>::THREADS, 0, s>>>(
-            x, r, p, w2, E, make_box_flat(bx), state, nullptr, rs);
+        cg_update2_kernel<NV, true><<<upd_grid<NV>(E), kRowThreads, 0, s>>>(
+            w, r, E, bx, state, nullptr, rs, bottom_totals, top_totals);
         SEM_CHECK_LAUNCH("sem_cg_update_slab launch");
         return 0;
     });

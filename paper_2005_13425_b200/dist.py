@@ -6,16 +6,24 @@ reference's element order e = ix + ex*(iy + ey*iz) (sembench/assembly.py:
 layers [z0, z1) and its local fields are exactly the slice [z0*ex*ey,
 z1*ex*ey) of the global arrays.
 
-Per CG iteration (the recurrence of sembench/cg.py:148-186):
+Per CG iteration (the recurrence of sembench/cg.py:148-186), the single-GPU
+solver's two kernels per rank (csrc/cg.cu):
 
-    p = beta p + r                      local                      (sem_cg_p)
-    w = A_local p                       local                      (sem_ax)
+    Ax launch(es): x += alpha_prev p_old (owed from the previous
+        iteration), p = beta p + r, w = A_local p, local sum of p.(A_local p)
+        -- bottom/top element layers first, the interior overlapping the
+        first halo step                                       (sem_cg_ax_slab)
     halo, step 1: top-face partial sums  -> rank r+1               (plane_top)
     halo, step 2: continue the prefix with own bottom-face copies
                   -> interface totals    -> rank r-1               (plane_bottom)
-    w2 = mask(dssum(w)) with the faces taken from the totals,
-         local <p, w2>_c partial        -> all_gather -> alpha     (assemble, finish)
-    x += alpha p, r -= alpha w2, local <r, r>_c -> all_gather       (update, finish)
+    all_gather of the <p, A p> partials -> alpha                    (finish 1)
+    r -= alpha mask(dssum(w)) with the faces taken from the totals,
+         local <r, r>_c partial -> all_gather                (update, finish 2)
+
+and after the loop the owed x += alpha p (sem_cg_finalize).  <p, A p> is the
+sum over elements of p.(A_local p), each element owned by exactly one rank,
+so the rank partials need no halo (p is continuous and masked; see
+ax_pencil.cuh).
 
 The two-step halo reproduces the reference's bincount order bit-for-bit:
 every copy on rank r-1's side of an interface has a lower element id than
@@ -220,11 +228,9 @@ class CudaSlabOps:
         check(self.lib.sem_cg_finish(dv.ptr(self.state), dv.ptr(gathered), gathered.numel(),
                                      phase, dv.ptr(self.history), self._s()), "dist cg finish")
 
-    def p_update(self) -> None:
-        """p = beta p + r is fused into the Ax launch (sem_cg_ax) below."""
-
-    def ax_layers(self, l0: int, l1: int) -> None:
-        """p = beta p + r and w = A_local p on the slab's element layers [l0, l1)."""
+    def ax_layers(self, l0: int, l1: int, first: bool) -> None:
+        """Iteration head + w = A_local p + <p, A p> partial on element layers
+        [l0, l1) (`first`: the iteration's first range resets the partial)."""
         p = self.part
         if l1 <= l0:
             return
@@ -232,13 +238,12 @@ class CudaSlabOps:
         e0, ne = l0 * per, (l1 - l0) * per
         off = lambda t, width: ctypes.c_void_p(t.data_ptr() + e0 * width * 8)  # noqa: E731
         nnn = p.n ** 3
-        check(self.lib.sem_cg_ax(off(self.p, nnn), off(self.r, nnn), off(self.g, 6 * nnn),
-                                 dv.host_f64_ptr(self.dx), dv.host_f64_ptr(self.dxt),
-                                 off(self.w, nnn), ne, p.n, dv.ptr(self.state),
-                                 dv.ptr(self.history), self._s()), "dist cg ax")
-
-    def ax(self) -> None:
-        self.ax_layers(0, self.part.ez)
+        check(self.lib.sem_cg_ax_slab(off(self.p, nnn), off(self.r, nnn), off(self.x, nnn),
+                                      off(self.g, 6 * nnn), dv.host_f64_ptr(self.dx),
+                                      dv.host_f64_ptr(self.dxt), off(self.w, nnn), ne, p.n,
+                                      dv.ptr(self.state), dv.ptr(self.history),
+                                      dv.ptr(self.w2), dv.ptr(self.scratch), 0 if first else 1,
+                                      self._s()), "dist cg ax")
 
     def plane_top(self, field: torch.Tensor) -> torch.Tensor:
         p = self.part
@@ -263,17 +268,17 @@ class CudaSlabOps:
                                       1 if apply_mask else 0, self._s()), "dist dssum")
         return out
 
-    def assemble(self, bottom_totals, top_totals) -> None:
+    def update(self, bottom_totals, top_totals) -> None:
+        """r -= alpha mask(dssum(w)) (faces from the halo totals); <r,r>_c partial."""
         ptr = lambda t: dv.ptr(t) if t is not None else ctypes.c_void_p(0)  # noqa: E731
-        check(self.lib.sem_cg_assemble_slab(dv.ptr(self.w), dv.ptr(self.w2), dv.ptr(self.p),
-                                            ptr(bottom_totals), ptr(top_totals),
-                                            dv.ptr(self.state), *self._slab(),
-                                            dv.ptr(self.scratch), self._s()), "dist assemble")
-
-    def update(self) -> None:
-        check(self.lib.sem_cg_update_slab(dv.ptr(self.x), dv.ptr(self.r), dv.ptr(self.p),
-                                          dv.ptr(self.w2), dv.ptr(self.state), *self._slab(),
+        check(self.lib.sem_cg_update_slab(dv.ptr(self.w), dv.ptr(self.r), ptr(bottom_totals),
+                                          ptr(top_totals), dv.ptr(self.state), *self._slab(),
                                           dv.ptr(self.scratch), self._s()), "dist update")
+
+    def finalize(self) -> None:
+        """The owed x += alpha p of the last iteration run."""
+        check(self.lib.sem_cg_finalize(dv.ptr(self.x), dv.ptr(self.p), dv.ptr(self.state),
+                                       self.x.numel(), self._s()), "dist finalize")
 
     def scalar_buffer(self, world: int) -> torch.Tensor:
         return torch.zeros(world, dtype=torch.float64, device=self.dev)
@@ -328,15 +333,15 @@ def dist_cg_solve(ops, comm: SlabComm, f_local, max_iterations: int, tolerance: 
     # the operator there first and overlap the interior with the first exchange
     edge = [(0, 1)] if ez == 1 else [(0, 1), (ez - 1, ez)]
     for _ in range(max_iterations):
-        ops.p_update()
-        for l0, l1 in edge:
-            ops.ax_layers(l0, l1)
+        for q, (l0, l1) in enumerate(edge):
+            ops.ax_layers(l0, l1, first=(q == 0))
         bot, top = halo_exchange(ops, comm, ops.w,
-                                 overlap=lambda: ops.ax_layers(1, ez - 1) if ez > 2 else None)
-        ops.assemble(bot, top)
+                                 overlap=lambda: ops.ax_layers(1, ez - 1, first=False)
+                                 if ez > 2 else None)
         ops.finish(1, comm.allgather(ops.local_sum(), gathered))
-        ops.update()
+        ops.update(bot, top)
         ops.finish(2, comm.allgather(ops.local_sum(), gathered))
+    ops.finalize()
     x, hist, iters, stop, pap, bit = ops.result()
     if stop == 2:
         from .cg import CgBreakdownError

@@ -24,7 +24,8 @@ from paper_2005_13425_b200.dist import (SlabComm, SlabPartition, dist_cg_solve, 
 
 class NumpySlabOps:
     """Per-rank compute in numpy, mirroring CudaSlabOps' interface and the
-    device kernels' scalar semantics (csrc/cg.cu fin_* functions)."""
+    device kernels' scalar semantics (csrc/cg.cu fin_* functions, the fused
+    Ax prologue/epilogue of ax_pencil.cuh)."""
 
     def __init__(self, part: SlabPartition, g_global, dx, dxt, topo_global, max_iterations):
         self.part = part
@@ -52,7 +53,7 @@ class NumpySlabOps:
         self.top_totals = torch.zeros(ps, dtype=torch.float64)
         self.history = np.zeros(max_iterations)
         self.st = dict(rtz=0.0, rtz_old=1.0, pap=0.0, alpha=0.0, it=0, iters=0, stop=0,
-                       bit=0, tol=0.0)
+                       bit=0, tol=0.0, xpend=False)
         self.local = torch.zeros(1, dtype=torch.float64)
 
     def scalar_buffer(self, world):
@@ -82,6 +83,7 @@ class NumpySlabOps:
             st.update(rtz=total, rtz_old=1.0, it=0, iters=0, stop=0)
         elif phase == 1:
             st["pap"] = total
+            st["xpend"] = False
             if total <= 0.0:
                 st["stop"], st["bit"] = 2, st["it"] + 1
             else:
@@ -90,13 +92,15 @@ class NumpySlabOps:
             it = st["it"] + 1
             rn = math.sqrt(total)
             self.history[it - 1] = rn
-            st.update(iters=it, rtz_old=st["rtz"], rtz=total, it=it)
+            st.update(iters=it, rtz_old=st["rtz"], rtz=total, it=it, xpend=True)
             if st["tol"] > 0.0 and rn < st["tol"]:
                 st["stop"] = 3
 
-    def p_update(self):
+    def ax_layers(self, l0, l1, first):
+        """Mirror of sem_cg_ax_slab: owed x update, p = beta p + r, w = A_local p
+        and the local sum of p.(A_local p) on element layers [l0, l1)."""
         st = self.st
-        if st["stop"]:
+        if l1 <= l0 or st["stop"]:
             return
         it = st["it"] + 1
         if st["rtz"] == 0.0:
@@ -104,17 +108,26 @@ class NumpySlabOps:
             st.update(iters=it, stop=1)
             return
         beta = 0.0 if it == 1 else st["rtz"] / st["rtz_old"]
-        O.scale_add(self.p, self.r, beta)
-
-    def ax_layers(self, l0, l1):
-        if l1 <= l0:
-            return
         if not hasattr(self, "w") or self.w is None or self.w.shape != self.p.shape:
             self.w = np.zeros_like(self.p)
         per = self.part.ex * self.part.ey
         a, b = l0 * per, l1 * per
-        self.w[a:b] = O.ax_layered(np.ascontiguousarray(self.p[a:b]), self.g[a:b], self.dx,
-                                   self.dxt)
+        if st["xpend"]:
+            xs = np.ascontiguousarray(self.x[a:b])
+            O.axpy_into(xs, np.ascontiguousarray(self.p[a:b]), st["alpha"])
+            self.x[a:b] = xs
+        ps = np.ascontiguousarray(self.p[a:b])
+        O.scale_add(ps, np.ascontiguousarray(self.r[a:b]), beta)
+        self.p[a:b] = ps
+        self.w[a:b] = O.ax_layered(ps, self.g[a:b], self.dx, self.dxt)
+        part = float(np.sum(ps * self.w[a:b]))
+        self.local[0] = part if first else float(self.local[0]) + part
+
+    def finalize(self):
+        st = self.st
+        if st["xpend"] and st["stop"] != 2:
+            O.axpy_into(self.x, self.p, st["alpha"])
+            st["xpend"] = False
 
     def _plane(self, field, sel, prefix):
         acc = np.zeros(self.part.plane_size) if prefix is None else prefix.numpy().copy()
@@ -138,18 +151,12 @@ class NumpySlabOps:
             out[self.on_top] = top.numpy()[self.plane_idx[self.on_top]]
         return out * self.maskv if apply_mask else out
 
-    def assemble(self, bot, top):
-        if self.st["stop"]:
-            return
-        self.w2 = self.dssum(self.w, bot, top, apply_mask=True)
-        self.local[0] = self._wdot(self.p, self.w2)
-
-    def update(self):
+    def update(self, bot, top):
         if self.st["stop"]:
             return
         a = self.st["alpha"]
-        O.axpy_into(self.x, self.p, a)
-        O.axpy_into(self.r, np.ascontiguousarray(self.w2), -a)
+        w2 = self.dssum(self.w, bot, top, apply_mask=True)
+        O.axpy_into(self.r, np.ascontiguousarray(w2), -a)
         self.local[0] = self._wdot(self.r, self.r)
 
     def result(self):
