@@ -305,6 +305,15 @@ def run_ours(args, rank, world, local_rank):
     cg_weak = None
     if args.cg_weak:
         cg_weak = bench_cg_weak(sb, dev, world, rank, args.cg_weak_iters)
+    cg_slab1 = None
+    if args.cg_slab1 and world == 1:
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29571")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        cg_slab1 = bench_cg_weak(sb, dev, 1, 0, args.cg_weak_iters, force_slab=True)
+        dist.destroy_process_group()
 
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ax_ncu_summary.json")
@@ -352,6 +361,8 @@ def run_ours(args, rank, world, local_rank):
             line["cg_e4096_p9"] = cg
         if cg_weak is not None:
             line["cg_weak_e32768_per_gpu"] = cg_weak
+        if cg_slab1 is not None:
+            line["cg_slab_solver_1gpu"] = cg_slab1
         print(json.dumps(line), flush=True)
     return 0
 
@@ -412,9 +423,10 @@ def bench_cg(sb, dev, iters):
                     "timed with CUDA events incl. one host sync at the end"}
 
 
-def bench_cg_weak(sb, dev, world, rank, iters):
+def bench_cg_weak(sb, dev, world, rank, iters, force_slab=False):
     """Weak-scaled CG: E=32768 per GPU, p=9, global box factor_elements(32768*G)
-    split into z-slabs (dist.py).  G=1 runs the fused single-GPU solver."""
+    split into z-slabs (dist.py).  G=1 runs the fused single-GPU solver
+    (force_slab: the slab solver instead, to compare per-rank cost)."""
     import torch
     import torch.distributed as dist
     from paper_2005_13425_b200 import perf
@@ -424,7 +436,7 @@ def bench_cg_weak(sb, dev, world, rank, iters):
     b = sb.build_basis(n)
     e_total = ex * ey * ez
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world == 1:
+    if world == 1 and not force_slab:
         mesh = sb.build_mesh(ex, ey, ez, n, 1.0)
         topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b, device=dev)
         f = sb.make_rhs(e_total, n, topo, sb.mix64(1, e_total), device=dev)
@@ -491,6 +503,8 @@ def main(argv=None):
     ap.add_argument("--cg", type=int, default=1)
     ap.add_argument("--cg-weak", type=int, default=1)
     ap.add_argument("--cg-weak-iters", type=int, default=100)
+    ap.add_argument("--cg-slab1", action="store_true",
+                    help="also time the multi-GPU slab solver on 1 GPU (NCCL world of 1)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
