@@ -306,7 +306,7 @@ static bool fill_dparam(DParamP<N>& P, const double* dx)
     return dev <= 1e-13 * scale;
 }
 
-template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
+template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0, int GMODE = 0,
           bool FOLD = false, int CGM = 0>
 static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
                          int64_t E, cudaStream_t stream, CgpArgs cgp = CgpArgs{})
@@ -345,13 +345,14 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     const int64_t resident = (int64_t)sm_count() * MINB;
     const int64_t grid = PERSIST ? (nbatches < resident ? nbatches : resident) : nbatches;
     // prefetch distance: the batch that replaces this one on its SM
-    const int64_t pf = (nbatches > resident) ? resident * SLOTS : 0;
+    int64_t pf = L2PF == 2 ? 0 : ((nbatches > resident) ? resident * SLOTS : -1);
+    if (const char* env = getenv("SEM_AX_PFDIST")) pf = atoll(env);  // tuning probe
     kern<<<(unsigned)grid, THREADS, SMEM, stream>>>(u, g, w, E, D, pf, cgp);
     SEM_CHECK_LAUNCH("sem_ax (pencil) launch");
     return 0;
 }
 
-template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false, int GMODE = 0,
+template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0, int GMODE = 0,
           bool FOLD = false, int CGM = 0>
 static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
                       cudaStream_t stream, CgpArgs cgp = CgpArgs{})
@@ -371,8 +372,10 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 // 2..19: pencil tuning points <elements per CTA, CTAs per SM, metric
 // prefetch depth, persistent, L2 bulk prefetch>.
 // Default tuning point per n (tools/ax_sweep.py on B200, E=4096; see
-// profiles/r01_ax_sweep.txt, CUDA-graph timed): index = n, value = variant id.
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 24, 46, 42, 46, 43};
+// profiles/r01_ax_sweep.txt, r01_ax_sweep_self_pf_raw.jsonl, CUDA-graph
+// timed): index = n, value = variant id.  n >= 12: folded register ring with
+// the CTA's own element bulk-prefetched into L2 at start (+10..30%).
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 50, 48, 48, 47, 48};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
@@ -412,6 +415,14 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
         case 44: return try_pencil<N, 1, 2, false, 1, true, 0, true>(u, g, dx, w, E, stream);
         case 45: return try_pencil<N, 1, 3, false, 1, false, 0, true>(u, g, dx, w, E, stream);
         case 46: return try_pencil<N, 1, 1, false, 2, false, 0, true>(u, g, dx, w, E, stream);
+        // large n: register ring + the CTA's own element bulk-prefetched to L2
+        case 47: return try_pencil<N, 1, 2, false, 1, 2, 0, true>(u, g, dx, w, E, stream);
+        case 48: return try_pencil<N, 1, 2, false, 2, 2, 0, true>(u, g, dx, w, E, stream);
+        case 49: return try_pencil<N, 1, 2, false, 1, 2, 0, false>(u, g, dx, w, E, stream);
+        case 50: return try_pencil<N, 1, 3, false, 1, 2, 0, true>(u, g, dx, w, E, stream);
+        case 51: return try_pencil<N, 1, 1, false, 3, 2, 0, true>(u, g, dx, w, E, stream);
+        case 52: return try_pencil<N, 1, 3, false, 1, 2, 1, true>(u, g, dx, w, E, stream);
+        case 53: return try_pencil<N, 1, 2, false, 1, 2, 1, true>(u, g, dx, w, E, stream);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
@@ -467,6 +478,8 @@ static int ax_cg_n(const double* g, const double* dx, double* w, int64_t E, CgpA
         return try_pencil<N, 1, 3, false, 1, true, 1, true, CGM>(p, g, dx, w, E, s, a);
     else if constexpr (N == 4)
         return try_pencil<N, 1, 2, false, 1, false, 1, false, CGM>(p, g, dx, w, E, s, a);
+    else if constexpr (N >= 12)  // register ring + own element prefetched to L2
+        return try_pencil<N, 1, 2, false, 2, 2, 0, true, CGM>(p, g, dx, w, E, s, a);
     else
         return try_pencil<N, 1, 2, false, 1, false, 0, false, CGM>(p, g, dx, w, E, s, a);
 }

@@ -206,7 +206,7 @@ struct CgpArgs {
     int accumulate;       // CGM == 3: add to (1) or reset (0) state->local_sum
 };
 
-template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, bool L2PF = false,
+template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0,
           int GMODE = 0, bool FOLD = false, int CGM = 0>
 __global__ void __launch_bounds__(THREADS, MINB)
 ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
@@ -354,7 +354,10 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                     gq[d][m] = (active && d < N) ? __ldg(ge + m * NNN + d * NN) : 0.0;
         }
         // warm L2 with the element this slot will process pf_elems later
-        if (L2PF && pf_elems > 0 && lane_ok && p == 0 && e + pf_elems < num_elements) {
+        // (L2PF 1: the one that replaces it a resident wave later; L2PF 2:
+        // pf_elems = 0, its own element -- the whole block is requested at
+        // once, so the register-ring loads that follow hit L2)
+        if (L2PF && pf_elems >= 0 && lane_ok && p == 0 && e + pf_elems < num_elements) {
             const int64_t en = e + pf_elems;
             prefetch_l2_bulk(u, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);
             if constexpr (CGM != 0) {
