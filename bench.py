@@ -297,6 +297,9 @@ def run_ours(args, rank, world, local_rank):
     assert w_host.device.type == "cpu"
     e2e_val = world * flops / e2e_s / 1e9
 
+    # ---- secondary: Ax at the paper's other sizes (BASELINE config 2) ----
+    ax_sizes = bench_ax_sizes(sb, dev, basis, stream) if (rank == 0 and args.ax_sizes) else None
+
     # ---- secondary: full Nekbone CG, 100 iterations (BASELINE config 4) ----
     cg = None
     if args.cg and rank == 0 and world == 1:
@@ -357,6 +360,8 @@ def run_ours(args, rank, world, local_rank):
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }
+        if ax_sizes is not None:
+            line["ax_e1024_e2048_p9"] = ax_sizes
         if cg is not None:
             line["cg_e4096_p9"] = cg
         if cg_weak is not None:
@@ -365,6 +370,50 @@ def run_ours(args, rank, world, local_rank):
             line["cg_slab_solver_1gpu"] = cg_slab1
         print(json.dumps(line), flush=True)
     return 0
+
+
+def bench_ax_sizes(sb, dev, basis, stream, steps=400):
+    """Ax at E = 1024 and 2048 (p = 9): enough rotating input sets that every
+    step streams from HBM (sets x 64 B x E n^3 >= 2 x L2), CUDA-graph
+    replays timed with CUDA events (burst clocks: a short region)."""
+    import torch
+    from paper_2005_13425_b200.kernels import apply_ax_into
+    from paper_2005_13425_b200.perf import measured_peaks
+    n = N_HEAD
+    hbm = float(measured_peaks(ROOT)["hbm_gbs"])
+    out = {}
+    for E in (1024, 2048):
+        nsets = max(2, -(-2 * 126 * 2 ** 20 // ax_bytes(E, n)))
+        sets = []
+        for s_ in range(nsets):
+            u = sb.random_field(E, n, 100 + s_, device=dev)
+            g = sb.random_field(6 * E, n, 200 + s_, device=dev).reshape(E, 6, n, n, n)
+            sets.append((u, g, torch.empty_like(u)))
+        for i in range(2 * nsets):
+            apply_ax_into(*sets[i % nsets][:2], basis, sets[i % nsets][2])
+        torch.cuda.synchronize(dev)
+        # one apply per input set captured in a CUDA graph (a 10 us kernel
+        # would otherwise wait on the Python launch path)
+        graph, side = torch.cuda.CUDAGraph(), torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side), torch.cuda.graph(graph, stream=side):
+            for u, g, w in sets:
+                apply_ax_into(u, g, basis, w)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        graph.replay()
+        torch.cuda.synchronize(dev)
+        reps = max(1, steps // nsets)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        us = e0.elapsed_time(e1) * 1e3 / (reps * nsets)
+        out[f"E{E}"] = {"us_per_apply": us, "gflops": ax_flops(E, n) / us / 1e3,
+                        "hbm_frac": ax_bytes(E, n) / (us * 1e3) / hbm, "input_sets": nsets}
+        del sets
+    return out
 
 
 def sustained_copy_us(dev, soak, steps):
@@ -501,6 +550,7 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cg", type=int, default=1)
+    ap.add_argument("--ax-sizes", type=int, default=1, help="also time E=1024/2048 (config 2)")
     ap.add_argument("--cg-weak", type=int, default=1)
     ap.add_argument("--cg-weak-iters", type=int, default=100)
     ap.add_argument("--cg-slab1", action="store_true",
