@@ -208,6 +208,19 @@ def test_ax_does_not_mutate_and_empty(cuda):
     assert np.array_equal(u, u0)
     w = sb.apply_ax(np.zeros((0, 6, 6, 6)), sb.GeomFactors(values=np.zeros((0, 6, 6, 6, 6))), b)
     assert w.shape == (0, 6, 6, 6)
+    # every variant and memory space: inputs untouched, empty inputs -> empty outputs
+    gd = sb.GeomFactors(values=torch.from_numpy(g).cuda())
+    for variant in ("reference", "scratch", "layered"):
+        for src in (u, torch.from_numpy(u).cuda(), torch.from_numpy(u).pin_memory()):
+            before = src.clone() if isinstance(src, torch.Tensor) else src.copy()
+            sb.apply_ax(src, gd, b, variant)
+            same = torch.equal(src.cpu(), before.cpu()) if isinstance(src, torch.Tensor) \
+                else np.array_equal(src, before)
+            assert same, variant
+        empty = sb.apply_ax(torch.zeros((0, 6, 6, 6), device="cuda"),
+                            sb.GeomFactors(values=torch.zeros((0, 6, 6, 6, 6), device="cuda")),
+                            b, variant)
+        assert tuple(empty.shape) == (0, 6, 6, 6)
 
 
 # ---------------------------------------------------------------- assembly --
