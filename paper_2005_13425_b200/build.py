@@ -50,6 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     objdir = tempfile.mkdtemp(prefix="libsem_obj_")
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    # tuning experiments: extra -D definitions (e.g. SEM_NVCC_DEFS="SEM_UPD_MINB=8")
+    compile_flags += [f"-D{d}" for d in os.environ.get("SEM_NVCC_DEFS", "").split()]
     if verbose:
         compile_flags += ["-Xptxas", "-v"]
     units = [(src, src.replace(".cu", ".o"), []) for src in SOURCES]

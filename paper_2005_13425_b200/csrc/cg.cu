@@ -27,6 +27,10 @@
 
 #include <algorithm>
 
+#ifndef SEM_UPD_MINB
+#define SEM_UPD_MINB 1
+#endif
+
 #include "box.cuh"
 #include "reduce.cuh"
 #include "flat.cuh"
@@ -255,7 +259,7 @@ static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_st
 // and <r, r>_c -> history, tolerance flag, beta's numerator (DIST: this
 // rank's partial -> state->local_sum, combined by sem_cg_finish).
 template <int N, bool DIST>
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(kRowThreads, SEM_UPD_MINB)
 cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, Box bx,
                   sem_cg_state* st, double* history, ReduceScratch* rs,
                   const double* __restrict__ bot, const double* __restrict__ top)
