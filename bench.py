@@ -176,11 +176,20 @@ def run_reference(args, rank, world):
     frac = min(1.0, budget / max(1e-9, (args.steps + args.warmup) * t_full))
     Es = max(1, int(E * frac))
     us, gs = np.ascontiguousarray(u[:Es]), np.ascontiguousarray(g[:Es])
-    for _ in range(args.warmup):
+    # warm-up: the W steps, and at least ~1 s so the thread pool and the
+    # cores' clocks have settled (the first calls of a fresh process run up
+    # to 1.5x slower)
+    t_w = time.perf_counter()
+    done = 0
+    while done < args.warmup or time.perf_counter() - t_w < 1.0:
         O.ax_layered(us, gs, b.diff, b.diff_t, threads)
+        done += 1
+    per = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
+        t1 = time.perf_counter()
         O.ax_layered(us, gs, b.diff, b.diff_t, threads)
+        per.append(time.perf_counter() - t1)
     dt = (time.perf_counter() - t0) / args.steps
     val = ax_flops(Es, N_HEAD) / dt / 1e9
     line = {
@@ -196,6 +205,8 @@ def run_reference(args, rank, world):
                                    f"cpu={_cpu_model()}"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
+        "step_ms": {"median": statistics.median(per) * 1e3, "min": min(per) * 1e3,
+                    "max": max(per) * 1e3, "warmup_calls": done},
     }
     print(json.dumps(line), flush=True)
     return 0

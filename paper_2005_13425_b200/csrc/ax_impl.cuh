@@ -27,6 +27,8 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <atomic>
+
 #include "sem_common.cuh"
 #include "ax_pencil.cuh"
 #include "box.cuh"
@@ -325,8 +327,13 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     }
     if (E == 0) return 0;
     auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGM>;
-    static bool configured = false;  // per template instance
-    if (!configured) {
+    // function attributes live in each device's context: configure once per
+    // (template instance, device); a benign race only repeats the setting
+    static std::atomic<uint64_t> configured{0};
+    int dev = 0;
+    if (cudaError_t err = cudaGetDevice(&dev)) return fail_cuda(err, "sem_ax: cudaGetDevice");
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)SMEM);
         if (err != cudaSuccess) return fail_cuda(err, "sem_ax: cudaFuncSetAttribute");
@@ -339,7 +346,7 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
             err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
             if (err != cudaSuccess) return fail_cuda(err, "sem_ax: carveout");
         }
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_release);
     }
     const int64_t nbatches = (E + SLOTS - 1) / SLOTS;
     const int64_t resident = (int64_t)sm_count() * MINB;
