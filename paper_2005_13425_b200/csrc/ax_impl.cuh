@@ -382,7 +382,7 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 // profiles/r01_ax_sweep.txt, r01_ax_sweep_self_pf_raw.jsonl, CUDA-graph
 // timed): index = n, value = variant id.  n >= 12: folded register ring with
 // the CTA's own element bulk-prefetched into L2 at start (+10..30%).
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 50, 48, 48, 47, 48};
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 50, 55, 55, 54, 48};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
@@ -430,6 +430,8 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
         case 51: return try_pencil<N, 1, 1, false, 3, 2, 0, true>(u, g, dx, w, E, stream);
         case 52: return try_pencil<N, 1, 3, false, 1, 2, 1, true>(u, g, dx, w, E, stream);
         case 53: return try_pencil<N, 1, 2, false, 1, 2, 1, true>(u, g, dx, w, E, stream);
+        case 54: return try_pencil<N, 1, 2, false, 3, 2, 0, true>(u, g, dx, w, E, stream);
+        case 55: return try_pencil<N, 1, 2, false, 4, 2, 0, true>(u, g, dx, w, E, stream);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
