@@ -31,6 +31,7 @@
 
 #include "sem_common.cuh"
 #include "ax_pencil.cuh"
+#include "ax_half.cuh"
 #include "box.cuh"
 
 namespace sem {
@@ -374,6 +375,42 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
             u, g, dx, w, E, stream, cgp);
 }
 
+// Half-pencil kernel (ax_half.cuh): two threads per k-pencil, large n.
+template <int N, int MINB, int PD, bool FOLD>
+static int launch_half(const double* u, const double* g, const double* dx, double* w, int64_t E,
+                       cudaStream_t stream)
+{
+    using C = HalfCfg<N>;
+    if constexpr (C::THREADS > 1024 || C::SMEM * MINB > 227 * 1024) {
+        return try_pencil<N, 1, 2, false, 2, 2, 0, true>(u, g, dx, w, E, stream);
+    } else {
+        DParamP<N> D;
+        const bool antisym = fill_dparam<N>(D, dx);
+        if constexpr (FOLD) {
+            if (!antisym) return launch_half<N, MINB, PD, false>(u, g, dx, w, E, stream);
+        }
+        if (E == 0) return 0;
+        if (E > 0x7fffffffLL) {
+            set_error("sem_ax: too many elements (%lld)", (long long)E);
+            return SEM_E_INVALID;
+        }
+        auto kern = ax_half_kernel<N, MINB, PD, FOLD>;
+        static std::atomic<uint64_t> configured{0};
+        int dev = 0;
+        if (cudaError_t err = cudaGetDevice(&dev)) return fail_cuda(err, "sem_ax: cudaGetDevice");
+        const uint64_t bit = 1ull << (dev & 63);
+        if (!(configured.load(std::memory_order_acquire) & bit)) {
+            cudaError_t err = cudaFuncSetAttribute(
+                kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+            if (err != cudaSuccess) return fail_cuda(err, "sem_ax: cudaFuncSetAttribute");
+            configured.fetch_or(bit, std::memory_order_release);
+        }
+        kern<<<(unsigned)E, C::THREADS, C::SMEM, stream>>>(u, g, w, E, D);
+        SEM_CHECK_LAUNCH("sem_ax (half-pencil) launch");
+        return 0;
+    }
+}
+
 // variant 0: the tuned default for this n (kDefaultVariant);
 // 1: per-point layered kernel (first B200 version, kept for ablation);
 // 2..19: pencil tuning points <elements per CTA, CTAs per SM, metric
@@ -382,7 +419,7 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 // profiles/r01_ax_sweep.txt, r01_ax_sweep_self_pf_raw.jsonl, CUDA-graph
 // timed): index = n, value = variant id.  n >= 12: folded register ring with
 // the CTA's own element bulk-prefetched into L2 at start (+10..30%).
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 50, 55, 55, 54, 48};
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 57, 55, 59, 54, 48};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
@@ -432,6 +469,12 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
         case 53: return try_pencil<N, 1, 2, false, 1, 2, 1, true>(u, g, dx, w, E, stream);
         case 54: return try_pencil<N, 1, 2, false, 3, 2, 0, true>(u, g, dx, w, E, stream);
         case 55: return try_pencil<N, 1, 2, false, 4, 2, 0, true>(u, g, dx, w, E, stream);
+        // half-pencil kernel (two threads per k-pencil)
+        case 56: return launch_half<N, 1, 2, true>(u, g, dx, w, E, stream);
+        case 57: return launch_half<N, 2, 2, true>(u, g, dx, w, E, stream);
+        case 58: return launch_half<N, 1, 3, true>(u, g, dx, w, E, stream);
+        case 59: return launch_half<N, 2, 1, true>(u, g, dx, w, E, stream);
+        case 60: return launch_half<N, 1, 4, true>(u, g, dx, w, E, stream);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
