@@ -58,6 +58,7 @@ extern "C" int sem_ax_variant(const double* u, const double* g, const double* dx
                               const double* dxt, double* w, int64_t num_elements,
                               int32_t n, int32_t variant, sem_stream_t stream)
 {
+    if (num_elements == 0) return 0;  // nothing to do; empty tensors may carry null pointers
     if (!u || !g || !dx || !dxt || !w || num_elements < 0) {
         sem::set_error("sem_ax: null pointer or negative element count");
         return SEM_E_INVALID;

@@ -214,6 +214,7 @@ extern "C" int sem_ax_reference(const double* u, const double* g, const double* 
                                 int64_t num_elements, int32_t n, sem_stream_t stream)
 {
     using namespace sem;
+    if (num_elements == 0) return 0;  // nothing to do; empty tensors may carry null pointers
     if (!u || !g || !dx || !dxt || !ur || !us || !ut || !w || num_elements < 0) {
         set_error("sem_ax_reference: null pointer or negative element count");
         return SEM_E_INVALID;
@@ -243,6 +244,7 @@ extern "C" int sem_ax_scratch(const double* u, const double* g, const double* dx
                               int64_t num_elements, int32_t n, sem_stream_t stream)
 {
     using namespace sem;
+    if (num_elements == 0) return 0;  // nothing to do; empty tensors may carry null pointers
     if (!u || !g || !dx || !w || num_elements < 0) {
         set_error("sem_ax_scratch: null pointer or negative element count");
         return SEM_E_INVALID;
