@@ -204,6 +204,9 @@ struct CgpArgs {
     double* partials;     // one double per CTA
     unsigned* counter;    // arrival counter (zero between launches)
     int accumulate;       // CGM == 3: add to (1) or reset (0) state->local_sum
+    int deferred;         // only publish the CTA partial (no fence / arrival
+                          // counter); cg_settle_kernel finishes the sum
+    unsigned* grid_out;   // host side: the launch's grid size (may be null)
 };
 
 template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0,
@@ -246,10 +249,41 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
 
     double beta = 0.0, alpha_prev = 0.0;
     bool xpend = false;
+    // GMODE 4: every bulk copy of the CTA (p, r, x, g) is issued before the
+    // CG scalars are read, so the state round trip overlaps the transfers;
+    // x is staged unconditionally (unused on the first iteration)
+    if constexpr (GMODE == 4) {
+        if (tid == 0) {
+            mbar_init(gbar, 1);
+            mbar_init(ubar, 1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int64_t e0 = batch;
+            mbar_expect_tx(ubar, (unsigned)(3 * NNN * 8));
+            for (int k = 0; k < N; ++k)
+                bulk_g2s(U + k * LSU, cgp.p + e0 * NNN + k * NN, NN * 8, ubar);
+            bulk_g2s(A, cgp.r + e0 * NNN, NNN * 8, ubar);
+            for (int k = 0; k < N; ++k)
+                bulk_g2s(B + k * LSB, cgp.x + e0 * NNN + k * NN, NN * 8, ubar);
+            mbar_expect_tx(gbar, (unsigned)(6 * NNN * 8));
+            bulk_g2s(Gbase, g + e0 * (6 * NNN), 6 * NNN * 8, gbar);
+        }
+    }
+    // a CTA must not retire with bulk copies into its shared memory in flight
+    auto drain = [&]() {
+        if constexpr (GMODE == 4) {
+            mbar_wait(ubar, 0);
+            mbar_wait(gbar, 0);
+        }
+    };
     if constexpr (CGM != 0) {
-        static_assert(!PERSIST && GMODE != 2, "CG fusion: one batch per CTA, u via registers");
+        static_assert(!PERSIST && GMODE != 2, "CG fusion: one batch per CTA, p via registers or GMODE 3");
         sem_cg_state* st = cgp.st;
-        if (st->stop) return;                       // uniform over the grid
+        if (st->stop) {                             // uniform over the grid
+            drain();
+            return;
+        }
         const int it = st->it + 1;
         const double rtz = st->rtz;
         if (rtz == 0.0) {                            // cg.py:151-158
@@ -258,6 +292,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                 st->iterations_run = it;
                 st->stop = 1;
             }
+            drain();
             return;
         }
         beta = (it == 1) ? 0.0 : rtz / st->rtz_old;
@@ -312,7 +347,9 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             for (int k = 0; k < N; ++k) ucol[k] = ok ? __ldg(src + k * NN) : 0.0;
         }
     };
-    if constexpr (GMODE != 2) load_ucol(batch);
+    static_assert(GMODE < 3 || (CGM != 0 && SLOTS == 1 && N % 2 == 0),
+                  "GMODE 3/4: CG fusion, one element per CTA, 16-byte layer copies");
+    if constexpr (GMODE < 2) load_ucol(batch);
 
     for (; batch < nbatches; batch += (PERSIST ? gridDim.x : nbatches)) {
         const int64_t e = batch * SLOTS + slot;
@@ -321,12 +358,12 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         // metric of layers 0..PD-1: issued first, in flight during S3/S1/S2
         double gq[GMODE ? 1 : PD][6];
         if constexpr (GMODE >= 1) {
-            if (tid == 0) {
+            if (GMODE != 4 && tid == 0) {
                 mbar_init(gbar, 1);
-                if (GMODE == 2) mbar_init(ubar, 1);
+                if (GMODE >= 2) mbar_init(ubar, 1);
             }
-            __syncthreads();
-            if (tid == 0) {
+            if constexpr (GMODE != 4) __syncthreads();
+            if (GMODE != 4 && tid == 0) {
                 const int64_t e0 = batch * SLOTS;
                 const int nact = (int)((num_elements - e0) < SLOTS ? (num_elements - e0) : SLOTS);
                 if constexpr (GMODE == 2) {
@@ -336,10 +373,40 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                             bulk_g2s(smem + (size_t)s2 * C::SLOT_DOUBLES + k * LSU,
                                      u + (e0 + s2) * NNN + k * NN, NN * 8, ubar);
                 }
+                if constexpr (GMODE == 3) {
+                    // CG operands first (needed at once), the metric after
+                    // (needed at S4): p_old -> U layers, r -> A, x -> B layers
+                    mbar_expect_tx(ubar, (unsigned)((xpend ? 3 : 2) * NNN * 8));
+                    for (int k = 0; k < N; ++k)
+                        bulk_g2s(U + k * LSU, cgp.p + e0 * NNN + k * NN, NN * 8, ubar);
+                    bulk_g2s(A, cgp.r + e0 * NNN, NNN * 8, ubar);
+                    if (xpend)
+                        for (int k = 0; k < N; ++k)
+                            bulk_g2s(B + k * LSB, cgp.x + e0 * NNN + k * NN, NN * 8, ubar);
+                }
                 mbar_expect_tx(gbar, (unsigned)(nact * 6 * NNN * 8));
                 for (int s2 = 0; s2 < nact; ++s2)
                     bulk_g2s(Gbase + (size_t)s2 * 6 * NNN, g + (e0 + s2) * (6 * NNN),
                              6 * NNN * 8, gbar);
+            }
+            if constexpr (GMODE >= 3) {
+                // iteration head from the staged operands (same arithmetic as
+                // load_ucol): x += alpha_prev p_old, p = beta p_old + r
+                mbar_wait(ubar, 0);
+                if (active) {
+                    const int64_t off = e * NNN + p;
+#pragma unroll
+                    for (int k = 0; k < N; ++k) {
+                        const double po = U[k * LSU + p];
+                        if (xpend)
+                            cgp.x[off + k * NN] = add_rn(B[k * LSB + p], mul_rn(alpha_prev, po));
+                        ucol[k] = add_rn(mul_rn(beta, po), A[k * LSA + p]);
+                        cgp.p[off + k * NN] = ucol[k];
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < N; ++k) ucol[k] = 0.0;
+                }
             }
             if constexpr (GMODE == 2) {
                 mbar_wait(ubar, 0);
@@ -522,6 +589,12 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         __shared__ double red_sh[THREADS / 32];
         __shared__ bool red_last;
         const double tot = block_sum<THREADS>(pap_acc, red_sh);
+        if (cgp.deferred) {
+            // the CTA retires at once: a per-CTA fence + atomic would hold
+            // its shared memory for a full memory round trip
+            if (tid == 0) cgp.partials[blockIdx.x] = tot;
+            return;
+        }
         if (tid == 0) {
             cgp.partials[blockIdx.x] = tot;
             __threadfence();

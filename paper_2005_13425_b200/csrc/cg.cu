@@ -28,7 +28,7 @@
 #include <algorithm>
 
 #ifndef SEM_UPD_MINB
-#define SEM_UPD_MINB 1
+#define SEM_UPD_MINB 6
 #endif
 
 #include "box.cuh"
@@ -226,19 +226,22 @@ static unsigned row_grid(int64_t E)
     return (unsigned)(blocks < kReduceBlocks ? (blocks > 0 ? blocks : 1) : kReduceBlocks);
 }
 
-// update2 grid: about four rows per thread, between kReduceBlocks and
-// kReduceBlocksMax blocks (tools/cg_tune.sh: at E = 4096 1184 blocks beat
-// one row per thread, at E = 32768 4736 blocks beat 1184 by 17%).  A
-// function of E and n only, so the reduction tree is fixed.
+// update2 grid: ONE full wave of the row kernel -- SEM_UPD_MINB (6) blocks
+// per SM x 148 SMs -- each thread walking its rows grid-stride (tools/
+// upd_minb2.sh, profiles/r01_cg_tune.txt: 888 blocks at 80 registers beat
+// 740 at 86 and 1184 / 1776 / 2368, i.e. 1.3-2 waves, by 10-25%).  A
+// constant (a function of E and n only, never of the device), so the
+// reduction tree is fixed.
+constexpr int kUpdBlocks = SEM_UPD_MINB * 148;
+static_assert(kUpdBlocks <= kReduceBlocksMax, "update grid exceeds the partial slots");
+
 template <int N>
 static unsigned upd_grid(int64_t E)
 {
     static const int cap = getenv("SEM_CG_UPD_BLOCKS") ? atoi(getenv("SEM_CG_UPD_BLOCKS")) : 0;
     const int64_t rows = E * N * N;
-    int64_t blocks = (rows + 4 * kRowThreads - 1) / (4 * kRowThreads);
-    blocks = std::max<int64_t>(blocks, std::min<int64_t>(kReduceBlocks, (rows + kRowThreads - 1) / kRowThreads));
-    blocks = std::min<int64_t>(blocks, kReduceBlocksMax);
-    if (cap > 0 && cap <= kReduceBlocksMax) blocks = std::min<int64_t>(blocks, cap);
+    int64_t blocks = std::min<int64_t>(kUpdBlocks, (rows + kRowThreads - 1) / kRowThreads);
+    if (cap > 0 && cap <= kReduceBlocksMax) blocks = std::min<int64_t>(rows, cap);
     return (unsigned)(blocks > 0 ? blocks : 1);
 }
 
@@ -262,7 +265,8 @@ template <int N, bool DIST>
 __global__ void __launch_bounds__(kRowThreads, SEM_UPD_MINB)
 cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, Box bx,
                   sem_cg_state* st, double* history, ReduceScratch* rs,
-                  const double* __restrict__ bot, const double* __restrict__ top)
+                  const double* __restrict__ bot, const double* __restrict__ top,
+                  bool deferred = false)
 {
     constexpr int NN = N * N, NNN = N * N * N;
     if (st->stop) return;
@@ -283,10 +287,175 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         store_row<N>(r + base, rv);
     }
     const double vals[1] = {acc};
+    if (deferred) {  // single GPU: cg_settle_kernel finishes <r, r>
+        reduce_publish_only<1, kRowThreads>(vals, rs);
+        return;
+    }
     reduce_publish_and_finish<1, kRowThreads>(vals, rs, [&](const double (&t)[1]) {
         if (DIST) st->local_sum = t[0];
         else fin_rr(st, t[0], history);
     });
+}
+
+// Flat-pair form of the iteration tail (same arithmetic, same ordered
+// gather): thread q owns the point pair (2q, 2q+1) of one row (n even; one
+// point for odd n), so the own w / r loads and the r store are fully
+// coalesced 128-bit accesses, and every copy of the pair's points -- up to
+// 2 x 2 (z, y) copies, each with its x-neighbour scalars -- is loaded
+// up-front under predicates before any addition consumes it, so all of a
+// thread's loads are in flight at once.  The sums then run in the
+// reference's ascending-element order: (z, y) copies lexicographically,
+// within each the x-lower copy, the own-x copy, the x-upper copy.
+template <int N, bool DIST>
+__global__ void __launch_bounds__(PairCfg<N>::THREADS)
+cg_update3_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, BoxFlat bf,
+                  sem_cg_state* st, double* history, ReduceScratch* rs,
+                  const double* __restrict__ bot, const double* __restrict__ top)
+{
+    constexpr int NNN = N * N * N;
+    if (st->stop) return;
+    const double nalpha = -st->alpha;
+    const Box& b = bf.b;
+    double acc = 0.0;
+    SEM_PAIR_LOOP(E) {
+        const int64_t q0 = u_ * NP;
+        ElemCoord c;
+        int i, j, k;
+        pair_point<N>(q0, bf, c, i, j, k);
+        double rv[NP];
+        ld_pair_rw<N>(r + q0, rv);
+        const AxisCopies ay = axis_copies<N>(c.iy, j, b.ey);
+        const AxisCopies az = axis_copies<N>(c.iz, k, b.ez);
+        bool xlo[NP], xhi[NP];
+#pragma unroll
+        for (int h = 0; h < NP; ++h) {
+            xlo[h] = (i + h == 0) && c.ix > 0;
+            xhi[h] = (i + h == N - 1) && c.ix < b.ex - 1;
+        }
+        const double* plane = nullptr;
+        if (DIST) {
+            if (bot != nullptr && c.iz == 0 && k == 0) plane = bot;
+            if (top != nullptr && c.iz == b.ez - 1 && k == N - 1) plane = top;
+        }
+        // loads: copy (zc, yc) at source element e + dz*ex*ey + dy*ex
+        double s[2][2][NP], lo[2][2][NP], hi[2][2][NP];
+        const int64_t e_own = q0 / NNN;
+        const int64_t exy = (int64_t)b.ex * b.ey;
+#pragma unroll
+        for (int zc = 0; zc < 2; ++zc) {
+#pragma unroll
+            for (int yc = 0; yc < 2; ++yc) {
+                const bool ok = zc < az.cnt && yc < ay.cnt && plane == nullptr;
+                const int ez_ = zc ? az.e1 : az.e0, kk = zc ? az.l1 : az.l0;
+                const int ey_ = yc ? ay.e1 : ay.e0, jj = yc ? ay.l1 : ay.l0;
+                const int64_t e2 = e_own + (int64_t)(ez_ - c.iz) * exy + (int64_t)(ey_ - c.iy) * b.ex;
+                const double* src = w + e2 * NNN + (kk * N + jj) * N + i;
+                if (ok) {
+                    ld_pair<N>(src, s[zc][yc]);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < NP; ++h) s[zc][yc][h] = 0.0;
+                }
+#pragma unroll
+                for (int h = 0; h < NP; ++h) {
+                    lo[zc][yc][h] = (ok && xlo[h]) ? __ldg(src + h - NNN + (N - 1)) : 0.0;
+                    hi[zc][yc][h] = (ok && xhi[h]) ? __ldg(src + h + NNN - (N - 1)) : 0.0;
+                }
+            }
+        }
+        double v[NP];
+        if (DIST && plane != nullptr) {
+            const int nx = b.ex * (N - 1) + 1;
+            const double* pr = plane + (int64_t)(c.iy * (N - 1) + j) * nx + c.ix * (N - 1) + i;
+#pragma unroll
+            for (int h = 0; h < NP; ++h) v[h] = __ldg(pr + h);
+        } else {
+#pragma unroll
+            for (int h = 0; h < NP; ++h) v[h] = 0.0;
+#pragma unroll
+            for (int zc = 0; zc < 2; ++zc) {
+#pragma unroll
+                for (int yc = 0; yc < 2; ++yc) {
+                    if (zc < az.cnt && yc < ay.cnt) {
+#pragma unroll
+                        for (int h = 0; h < NP; ++h) {
+                            double t = v[h];
+                            if (xlo[h]) t = add_rn(t, lo[zc][yc][h]);
+                            t = add_rn(t, s[zc][yc][h]);
+                            if (xhi[h]) t = add_rn(t, hi[zc][yc][h]);
+                            v[h] = t;
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < NP; ++h) {
+            rv[h] = add_rn(rv[h], mul_rn(nalpha, mul_rn(v[h], mask_of<N>(c, i + h, j, k, b))));
+            acc += mul_rn(mul_rn(rv[h], rv[h]), inv_mult_of<N>(c, i + h, j, k, b));
+        }
+        st_pair<N>(r + q0, rv);
+    }
+    const double vals[1] = {acc};
+    reduce_publish_and_finish<1, PairCfg<N>::THREADS>(vals, rs, [&](const double (&t)[1]) {
+        if (DIST) st->local_sum = t[0];
+        else fin_rr(st, t[0], history);
+    });
+}
+
+// which tail kernel (tuning hook SEM_CG_UPD: 0 rows, 1 flat pairs)
+static int upd_kind()
+{
+    static const int k = getenv("SEM_CG_UPD") ? atoi(getenv("SEM_CG_UPD")) : 0;
+    return k;
+}
+
+template <int N>
+static unsigned upd3_grid(int64_t E)
+{
+    static const int cap = getenv("SEM_CG_UPD_BLOCKS") ? atoi(getenv("SEM_CG_UPD_BLOCKS")) : 0;
+    const int lim = (cap > 0 && cap <= kReduceBlocksMax) ? cap : kReduceBlocksMax;
+    return flat_grid<N>(E, lim);
+}
+
+template <int N, bool DIST>
+static void launch_update(const double* w, double* r, int64_t E, const Box& bx, sem_cg_state* st,
+                          double* history, ReduceScratch* rs, const double* bot,
+                          const double* top, cudaStream_t s)
+{
+    if (upd_kind() == 1)
+        cg_update3_kernel<N, DIST><<<upd3_grid<N>(E), PairCfg<N>::THREADS, 0, s>>>(
+            w, r, E, make_box_flat(bx), st, history, rs, bot, top);
+    else
+        cg_update2_kernel<N, DIST><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, bx, st, history,
+                                                                         rs, bot, top);
+}
+
+// Finish a deferred reduction of the single-GPU iteration: the fixed-order
+// sum of the launch's block partials, then the phase bookkeeping
+// (PH = kPhasePap: alpha / breakdown; PH = 2: rnorm history, beta's numerator).
+constexpr int kSettleThreads = 1024;
+// PH = kPhaseLocal (z-slab rank): add the sum to state->local_sum, or reset
+// it first (accumulate == 0).
+constexpr int kPhaseLocal = 3;
+template <int PH>
+__global__ void __launch_bounds__(kSettleThreads)
+cg_settle_kernel(const double* __restrict__ partials, int count, sem_cg_state* st,
+                 double* history, int accumulate = 0)
+{
+    if (st->stop) return;
+    const double tot = settle_sum<kSettleThreads>(partials, count);
+    if (threadIdx.x != 0) return;
+    if (PH == kPhaseLocal) st->local_sum = (accumulate ? st->local_sum : 0.0) + tot;
+    else fin_phase(st, PH, tot, history);
+}
+
+// tuning hook SEM_CG_FIN (0: fused reductions, 1: both deferred, 2: the Ax
+// reduction deferred only)
+static int fin_mode()
+{
+    static const int k = getenv("SEM_CG_FIN") ? atoi(getenv("SEM_CG_FIN")) : 2;
+    return k;
 }
 
 // The owed x += alpha p of the last iteration (every exit except breakdown).
@@ -314,14 +483,28 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
     auto mark = [&](int q) { return marks ? cudaEventRecord(marks[q], s) : cudaSuccess; };
     // w2 (the second half of the w scratch) holds the Ax kernel's per-CTA
     // <p, A p> partials (one per element at most)
-    const CgpArgs a{p, r, st, history, x, w2, &rs->counter};
+    const bool defer = fin_mode() == 1, defer_ax = fin_mode() >= 1;
+    unsigned ax_grid = 0;
+    const CgpArgs a{p, r, st, history, x, w2, &rs->counter, 0, defer_ax ? 1 : 0, &ax_grid};
     for (int it = 0; it < iters; ++it) {
         if (cudaError_t e = mark(3 * it)) return fail_cuda(e, "sem_cg_run: event");
         if (int rc = ax_cg_dispatch(g, dx, w, E, N, a, 2, s)) return rc;
+        if (defer_ax) {
+            cg_settle_kernel<kPhasePap><<<1, kSettleThreads, 0, s>>>(w2, (int)ax_grid, st, history);
+            SEM_CHECK_LAUNCH("cg settle (pap)");
+        }
         if (cudaError_t e = mark(3 * it + 1)) return fail_cuda(e, "sem_cg_run: event");
-        cg_update2_kernel<N, false><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, bx, st, history,
-                                                                          rs, nullptr, nullptr);
-        SEM_CHECK_LAUNCH("cg_update2_kernel");
+        if (defer) {
+            const unsigned ug = upd_grid<N>(E);
+            cg_update2_kernel<N, false><<<ug, kRowThreads, 0, s>>>(w, r, E, bx, st, history, rs,
+                                                                  nullptr, nullptr, true);
+            SEM_CHECK_LAUNCH("cg update kernel");
+            cg_settle_kernel<2><<<1, kSettleThreads, 0, s>>>(rs->partials[0], (int)ug, st, history);
+            SEM_CHECK_LAUNCH("cg settle (rr)");
+        } else {
+            launch_update<N, false>(w, r, E, bx, st, history, rs, nullptr, nullptr, s);
+        }
+        SEM_CHECK_LAUNCH("cg update kernel");
         if (cudaError_t e = mark(3 * it + 2)) return fail_cuda(e, "sem_cg_run: event");
     }
     if (cudaError_t e = mark(3 * iters)) return fail_cuda(e, "sem_cg_run: event");
@@ -574,8 +757,16 @@ extern "C" int sem_cg_ax_slab(double* p, const double* r, double* x, const doubl
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (int rc = bind_stream_device(s)) return rc;
     auto* rs = static_cast<ReduceScratch*>(scratch);
-    const CgpArgs a{p, r, state, history, x, partials, &rs->counter, accumulate ? 1 : 0};
-    return ax_cg_dispatch(g, dx, w, num_elements, n, a, 3, s);
+    // deferred <p, A p> partial: the CTAs only publish, one settle block sums
+    unsigned grid = 0;
+    const CgpArgs a{p, r, state, history, x, partials, &rs->counter, accumulate ? 1 : 0, 1,
+                    &grid};
+    if (num_elements == 0) return 0;
+    if (int rc = ax_cg_dispatch(g, dx, w, num_elements, n, a, 3, s)) return rc;
+    cg_settle_kernel<kPhaseLocal><<<1, kSettleThreads, 0, s>>>(partials, (int)grid, state, history,
+                                                               accumulate ? 1 : 0);
+    SEM_CHECK_LAUNCH("sem_cg_ax_slab settle");
+    return 0;
 }
 
 extern "C" int sem_cg_update_slab(const double* w, double* r, const double* bottom_totals,
@@ -594,8 +785,7 @@ extern "C" int sem_cg_update_slab(const double* w, double* r, const double* bott
     const int64_t E = (int64_t)ex * ey * ez;
     auto* rs = static_cast<ReduceScratch*>(scratch);
     SEM_SWITCH_N(n, {
-        cg_update2_kernel<NV, true><<<upd_grid<NV>(E), kRowThreads, 0, s>>>(
-            w, r, E, bx, state, nullptr, rs, bottom_totals, top_totals);
+        launch_update<NV, true>(w, r, E, bx, state, nullptr, rs, bottom_totals, top_totals, s);
         SEM_CHECK_LAUNCH("sem_cg_update_slab launch");
         return 0;
     });

@@ -84,4 +84,30 @@ __device__ __forceinline__ void reduce_publish_and_finish(const double (&vals)[N
     }
 }
 
+// Deferred form: publish this block's NR totals only (no fence, no arrival
+// counter, the block retires at once); a following kernel combines them.
+template <int NR, int THREADS>
+__device__ __forceinline__ void reduce_publish_only(const double (&vals)[NR], ReduceScratch* rs)
+{
+    __shared__ double sh[THREADS / 32];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+        const double t = block_sum<THREADS>(vals[q], sh);
+        if (threadIdx.x == 0) rs->partials[q][blockIdx.x] = t;
+    }
+}
+
+// Sum count partials in a fixed order with one block of THREADS threads
+// (every load independent, so the whole set is in flight at once); the
+// total is valid in thread 0.
+template <int THREADS>
+__device__ __forceinline__ double settle_sum(const double* __restrict__ partials, int count)
+{
+    __shared__ double sh[THREADS / 32];
+    double v = 0.0;
+#pragma unroll 16
+    for (int b = threadIdx.x; b < count; b += THREADS) v += __ldcg(partials + b);
+    return block_sum<THREADS>(v, sh);
+}
+
 }  // namespace sem
