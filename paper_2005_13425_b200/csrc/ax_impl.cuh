@@ -356,6 +356,12 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     int64_t pf = L2PF == 2 ? 0 : ((nbatches > resident) ? resident * SLOTS : -1);
     if (const char* env = getenv("SEM_AX_PFDIST")) pf = atoll(env);  // tuning probe
     if (cgp.grid_out) *cgp.grid_out = (unsigned)grid;
+    if (cgp.pdl) {
+        cudaError_t err = launch_k(kern, dim3((unsigned)grid), dim3(THREADS), SMEM, stream, true,
+                                   u, g, w, E, D, pf, cgp);
+        if (err != cudaSuccess) return fail_cuda(err, "sem_ax (pencil, PDL) launch");
+        return 0;
+    }
     kern<<<(unsigned)grid, THREADS, SMEM, stream>>>(u, g, w, E, D, pf, cgp);
     SEM_CHECK_LAUNCH("sem_ax (pencil) launch");
     return 0;

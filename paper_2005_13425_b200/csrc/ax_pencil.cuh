@@ -207,6 +207,8 @@ struct CgpArgs {
     int deferred;         // only publish the CTA partial (no fence / arrival
                           // counter); cg_settle_kernel finishes the sum
     unsigned* grid_out;   // host side: the launch's grid size (may be null)
+    int pdl;              // launched as a programmatic dependent (GMODE 4: the
+                          // metric copy is issued before griddep_wait)
 };
 
 template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0,
@@ -258,6 +260,13 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             mbar_init(ubar, 1);
         }
         __syncthreads();
+        // the metric is never written during a solve: its copy may start
+        // while the previous kernel of the iteration chain is still running
+        if (tid == 0) {
+            mbar_expect_tx(gbar, (unsigned)(6 * NNN * 8));
+            bulk_g2s(Gbase, g + batch * (6 * NNN), 6 * NNN * 8, gbar);
+        }
+        griddep_wait();
         if (tid == 0) {
             const int64_t e0 = batch;
             mbar_expect_tx(ubar, (unsigned)(3 * NNN * 8));
@@ -266,9 +275,9 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             bulk_g2s(A, cgp.r + e0 * NNN, NNN * 8, ubar);
             for (int k = 0; k < N; ++k)
                 bulk_g2s(B + k * LSB, cgp.x + e0 * NNN + k * NN, NN * 8, ubar);
-            mbar_expect_tx(gbar, (unsigned)(6 * NNN * 8));
-            bulk_g2s(Gbase, g + e0 * (6 * NNN), 6 * NNN * 8, gbar);
         }
+    } else if constexpr (CGM != 0) {
+        griddep_wait();
     }
     // a CTA must not retire with bulk copies into its shared memory in flight
     auto drain = [&]() {
@@ -588,6 +597,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         // arrive sums them in a fixed order and settles alpha (cg.py:163-170)
         __shared__ double red_sh[THREADS / 32];
         __shared__ bool red_last;
+        griddep_launch();  // late trigger: the dependent launches as this grid drains
         const double tot = block_sum<THREADS>(pap_acc, red_sh);
         if (cgp.deferred) {
             // the CTA retires at once: a per-CTA fence + atomic would hold

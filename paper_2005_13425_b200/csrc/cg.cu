@@ -269,6 +269,7 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
                   bool deferred = false)
 {
     constexpr int NN = N * N, NNN = N * N * N;
+    griddep_wait();
     if (st->stop) return;
     const double nalpha = -st->alpha;
     double acc = 0.0;
@@ -286,6 +287,7 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         }
         store_row<N>(r + base, rv);
     }
+    griddep_launch();
     const double vals[1] = {acc};
     if (deferred) {  // single GPU: cg_settle_kernel finishes <r, r>
         reduce_publish_only<1, kRowThreads>(vals, rs);
@@ -443,6 +445,8 @@ __global__ void __launch_bounds__(kSettleThreads)
 cg_settle_kernel(const double* __restrict__ partials, int count, sem_cg_state* st,
                  double* history, int accumulate = 0)
 {
+    griddep_wait();
+    griddep_launch();
     if (st->stop) return;
     const double tot = settle_sum<kSettleThreads>(partials, count);
     if (threadIdx.x != 0) return;
@@ -456,6 +460,12 @@ static int fin_mode()
 {
     static const int k = getenv("SEM_CG_FIN") ? atoi(getenv("SEM_CG_FIN")) : 2;
     return k;
+}
+// programmatic dependent launch of the iteration chain (SEM_CG_PDL=1 enables)
+static bool cg_pdl()
+{
+    static const int k = getenv("SEM_CG_PDL") ? atoi(getenv("SEM_CG_PDL")) : 0;
+    return k != 0;
 }
 
 // The owed x += alpha p of the last iteration (every exit except breakdown).
@@ -484,25 +494,43 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
     // w2 (the second half of the w scratch) holds the Ax kernel's per-CTA
     // <p, A p> partials (one per element at most)
     const bool defer = fin_mode() == 1, defer_ax = fin_mode() >= 1;
+    // PDL chain (no phase events in between): each kernel may launch while
+    // its predecessor drains and waits on it in-kernel (griddep_wait)
+    const bool pdl = cg_pdl() && marks == nullptr;
     unsigned ax_grid = 0;
-    const CgpArgs a{p, r, st, history, x, w2, &rs->counter, 0, defer_ax ? 1 : 0, &ax_grid};
+    const CgpArgs a{p, r, st, history, x, w2, &rs->counter, 0, defer_ax ? 1 : 0, &ax_grid,
+                    pdl ? 1 : 0};
+    auto chk = [](cudaError_t e, const char* what) { return e == cudaSuccess ? 0 : fail_cuda(e, what); };
     for (int it = 0; it < iters; ++it) {
         if (cudaError_t e = mark(3 * it)) return fail_cuda(e, "sem_cg_run: event");
         if (int rc = ax_cg_dispatch(g, dx, w, E, N, a, 2, s)) return rc;
         if (defer_ax) {
-            cg_settle_kernel<kPhasePap><<<1, kSettleThreads, 0, s>>>(w2, (int)ax_grid, st, history);
-            SEM_CHECK_LAUNCH("cg settle (pap)");
+            if (int rc = chk(launch_k(cg_settle_kernel<kPhasePap>, dim3(1), dim3(kSettleThreads), 0, s,
+                                      pdl, (const double*)w2, (int)ax_grid, st, history, 0),
+                             "cg settle (pap)"))
+                return rc;
         }
         if (cudaError_t e = mark(3 * it + 1)) return fail_cuda(e, "sem_cg_run: event");
         if (defer) {
             const unsigned ug = upd_grid<N>(E);
-            cg_update2_kernel<N, false><<<ug, kRowThreads, 0, s>>>(w, r, E, bx, st, history, rs,
-                                                                  nullptr, nullptr, true);
-            SEM_CHECK_LAUNCH("cg update kernel");
-            cg_settle_kernel<2><<<1, kSettleThreads, 0, s>>>(rs->partials[0], (int)ug, st, history);
-            SEM_CHECK_LAUNCH("cg settle (rr)");
-        } else {
+            if (int rc = chk(launch_k(cg_update2_kernel<N, false>, dim3(ug), dim3(kRowThreads), 0, s,
+                                      pdl, (const double*)w, r, E, bx, st, history, rs,
+                                      (const double*)nullptr, (const double*)nullptr, true),
+                             "cg update kernel"))
+                return rc;
+            if (int rc = chk(launch_k(cg_settle_kernel<2>, dim3(1), dim3(kSettleThreads), 0, s, pdl,
+                                      (const double*)rs->partials[0], (int)ug, st, history, 0),
+                             "cg settle (rr)"))
+                return rc;
+        } else if (upd_kind() == 1) {
             launch_update<N, false>(w, r, E, bx, st, history, rs, nullptr, nullptr, s);
+        } else {
+            if (int rc = chk(launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
+                                      dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E, bx, st,
+                                      history, rs, (const double*)nullptr,
+                                      (const double*)nullptr, false),
+                             "cg update kernel"))
+                return rc;
         }
         SEM_CHECK_LAUNCH("cg update kernel");
         if (cudaError_t e = mark(3 * it + 2)) return fail_cuda(e, "sem_cg_run: event");
@@ -760,7 +788,7 @@ extern "C" int sem_cg_ax_slab(double* p, const double* r, double* x, const doubl
     // deferred <p, A p> partial: the CTAs only publish, one settle block sums
     unsigned grid = 0;
     const CgpArgs a{p, r, state, history, x, partials, &rs->counter, accumulate ? 1 : 0, 1,
-                    &grid};
+                    &grid, 0};
     if (num_elements == 0) return 0;
     if (int rc = ax_cg_dispatch(g, dx, w, num_elements, n, a, 3, s)) return rc;
     cg_settle_kernel<kPhaseLocal><<<1, kSettleThreads, 0, s>>>(partials, (int)grid, state, history,
