@@ -9,11 +9,12 @@
 // * The CG driver keeps rtz / pap / alpha / beta in a device-side
 //   sem_cg_state and never synchronises the host; early exits (rtz == 0,
 //   tolerance, breakdown) set a device stop flag that turns the remaining
-//   queued launches into no-ops.  Single GPU (sem_cg_run): TWO launches per
-//   iteration --
+//   queued launches into no-ops.  Single GPU (sem_cg_run): two streaming
+//   launches plus one single-block settle per iteration --
 //     1. Ax with the iteration head fused in (ax_pencil.cuh, CGM = 2):
 //        x += alpha_prev p_old (deferred from the previous iteration),
-//        p = beta p + r, w = A_local p, <p, A p> -> alpha;
+//        p = beta p + r, w = A_local p, per-CTA partials of <p, A p>;
+//     1b. cg_settle_kernel: the partials in a fixed order -> alpha;
 //     2. cg_update2_kernel: r += (-alpha) mask(dssum(w)) with the ordered
 //        dssum gathered per row, and <r, r>_c -> rnorm, beta's numerator;
 //   and sem_cg_finalize applies the last pending x update.  120 B per point
