@@ -462,11 +462,14 @@ static int fin_mode()
     static const int k = getenv("SEM_CG_FIN") ? atoi(getenv("SEM_CG_FIN")) : 2;
     return k;
 }
-// programmatic dependent launch of the iteration chain (SEM_CG_PDL=1 enables)
-static bool cg_pdl()
+// programmatic dependent launch of the iteration chain (SEM_CG_PDL: 0 off,
+// 1 every launch, 2 (default) the settle and update launches only: they are
+// small / register-only, so launching them while the Ax grid drains costs it
+// no residency; tools/cg_tune7.sh: E = 4096 96.3 -> 95.0 us per iteration)
+static int cg_pdl()
 {
-    static const int k = getenv("SEM_CG_PDL") ? atoi(getenv("SEM_CG_PDL")) : 0;
-    return k != 0;
+    static const int k = getenv("SEM_CG_PDL") ? atoi(getenv("SEM_CG_PDL")) : 2;
+    return k;
 }
 
 // The owed x += alpha p of the last iteration (every exit except breakdown).
@@ -497,10 +500,11 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
     const bool defer = fin_mode() == 1, defer_ax = fin_mode() >= 1;
     // PDL chain (no phase events in between): each kernel may launch while
     // its predecessor drains and waits on it in-kernel (griddep_wait)
-    const bool pdl = cg_pdl() && marks == nullptr;
+    // (SEM_CG_PDL=1: every launch; 2: the settle and update launches only)
+    const bool pdl = cg_pdl() != 0 && marks == nullptr;
     unsigned ax_grid = 0;
     const CgpArgs a{p, r, st, history, x, w2, &rs->counter, 0, defer_ax ? 1 : 0, &ax_grid,
-                    pdl ? 1 : 0};
+                    (pdl && cg_pdl() == 1) ? 1 : 0};
     auto chk = [](cudaError_t e, const char* what) { return e == cudaSuccess ? 0 : fail_cuda(e, what); };
     for (int it = 0; it < iters; ++it) {
         if (cudaError_t e = mark(3 * it)) return fail_cuda(e, "sem_cg_run: event");

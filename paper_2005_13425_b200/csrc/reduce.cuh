@@ -105,8 +105,15 @@ __device__ __forceinline__ double settle_sum(const double* __restrict__ partials
 {
     __shared__ double sh[THREADS / 32];
     double v = 0.0;
-#pragma unroll 16
-    for (int b = threadIdx.x; b < count; b += THREADS) v += __ldcg(partials + b);
+    // 128-bit loads (the partial arrays are 16-byte aligned)
+    const double2* p2 = reinterpret_cast<const double2*>(partials);
+#pragma unroll 4
+    for (int b = threadIdx.x; b < count / 2; b += THREADS) {
+        const double2 t = __ldcg(p2 + b);
+        v += t.x;
+        v += t.y;
+    }
+    if ((count & 1) && threadIdx.x == 0) v += __ldcg(partials + count - 1);
     return block_sum<THREADS>(v, sh);
 }
 
