@@ -237,11 +237,11 @@ constexpr int kUpdBlocks = SEM_UPD_MINB * 148;
 static_assert(kUpdBlocks <= kReduceBlocksMax, "update grid exceeds the partial slots");
 
 template <int N>
-static unsigned upd_grid(int64_t E)
+static unsigned upd_grid(int64_t E, int wave = kUpdBlocks)
 {
     static const int cap = getenv("SEM_CG_UPD_BLOCKS") ? atoi(getenv("SEM_CG_UPD_BLOCKS")) : 0;
     const int64_t rows = E * N * N;
-    int64_t blocks = std::min<int64_t>(kUpdBlocks, (rows + kRowThreads - 1) / kRowThreads);
+    int64_t blocks = std::min<int64_t>(wave, (rows + kRowThreads - 1) / kRowThreads);
     if (cap > 0 && cap <= kReduceBlocksMax) blocks = std::min<int64_t>(rows, cap);
     return (unsigned)(blocks > 0 ? blocks : 1);
 }
@@ -294,6 +294,62 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         reduce_publish_only<1, kRowThreads>(vals, rs);
         return;
     }
+    reduce_publish_and_finish<1, kRowThreads>(vals, rs, [&](const double (&t)[1]) {
+        if (DIST) st->local_sum = t[0];
+        else fin_rr(st, t[0], history);
+    });
+}
+
+// Software-pipelined row tail (SEM_CG_UPD=2): the own w row and the r row
+// of the thread's NEXT grid-stride row are loaded before the current row is
+// assembled, so two rows' worth of loads are in flight per thread (more
+// registers: 4 blocks per SM, one wave = 4 x 148 blocks).
+#ifndef SEM_UPD4_MINB
+#define SEM_UPD4_MINB 4
+#endif
+constexpr int kUpd4MinB = SEM_UPD4_MINB;
+template <int N, bool DIST>
+__global__ void __launch_bounds__(kRowThreads, kUpd4MinB)
+cg_update4_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, Box bx,
+                  sem_cg_state* st, double* history, ReduceScratch* rs,
+                  const double* __restrict__ bot, const double* __restrict__ top)
+{
+    constexpr int NN = N * N;
+    griddep_wait();
+    if (st->stop) return;
+    const double nalpha = -st->alpha;
+    double acc = 0.0;
+    const int64_t rows = E * NN, stride = (int64_t)gridDim.x * kRowThreads;
+    int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x;
+    double wn[N], rn[N];
+    if (row < rows) {
+        load_row<N>(w + row * N, wn);
+        load_row_rw<N>(r + row * N, rn);
+    }
+    for (; row < rows; row += stride) {
+        double wc[N], rv[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            wc[i] = wn[i];
+            rv[i] = rn[i];
+        }
+        const int64_t nx = row + stride;
+        if (nx < rows) {
+            load_row<N>(w + nx * N, wn);
+            load_row_rw<N>(r + nx * N, rn);
+        }
+        const Row<N> rw = make_row<N>(row, bx);
+        double v[N];
+        dssum_row_own<N>(w, rw, bx, DIST ? bot : nullptr, DIST ? top : nullptr, wc, v);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            rv[i] = add_rn(rv[i], mul_rn(nalpha, mul_rn(v[i], row_mask<N>(rw, i))));
+            acc += mul_rn(mul_rn(rv[i], rv[i]), row_inv_mult<N>(rw, i));
+        }
+        store_row<N>(r + row * N, rv);
+    }
+    griddep_launch();
+    const double vals[1] = {acc};
     reduce_publish_and_finish<1, kRowThreads>(vals, rs, [&](const double (&t)[1]) {
         if (DIST) st->local_sum = t[0];
         else fin_rr(st, t[0], history);
@@ -406,7 +462,7 @@ cg_update3_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     });
 }
 
-// which tail kernel (tuning hook SEM_CG_UPD: 0 rows, 1 flat pairs)
+// which tail kernel (tuning hook SEM_CG_UPD: 0 rows, 1 flat pairs, 2 pipelined rows)
 static int upd_kind()
 {
     static const int k = getenv("SEM_CG_UPD") ? atoi(getenv("SEM_CG_UPD")) : 0;
@@ -429,6 +485,9 @@ static void launch_update(const double* w, double* r, int64_t E, const Box& bx, 
     if (upd_kind() == 1)
         cg_update3_kernel<N, DIST><<<upd3_grid<N>(E), PairCfg<N>::THREADS, 0, s>>>(
             w, r, E, make_box_flat(bx), st, history, rs, bot, top);
+    else if (upd_kind() == 2)
+        cg_update4_kernel<N, DIST><<<upd_grid<N>(E, kUpd4MinB * 148), kRowThreads, 0, s>>>(
+            w, r, E, bx, st, history, rs, bot, top);
     else
         cg_update2_kernel<N, DIST><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, bx, st, history,
                                                                          rs, bot, top);
@@ -527,7 +586,7 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
                                       (const double*)rs->partials[0], (int)ug, st, history, 0),
                              "cg settle (rr)"))
                 return rc;
-        } else if (upd_kind() == 1) {
+        } else if (upd_kind() != 0) {
             launch_update<N, false>(w, r, E, bx, st, history, rs, nullptr, nullptr, s);
         } else {
             if (int rc = chk(launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
