@@ -237,11 +237,11 @@ constexpr int kUpdBlocks = SEM_UPD_MINB * 148;
 static_assert(kUpdBlocks <= kReduceBlocksMax, "update grid exceeds the partial slots");
 
 template <int N>
-static unsigned upd_grid(int64_t E, int wave = kUpdBlocks)
+static unsigned upd_grid(int64_t E)
 {
     static const int cap = getenv("SEM_CG_UPD_BLOCKS") ? atoi(getenv("SEM_CG_UPD_BLOCKS")) : 0;
     const int64_t rows = E * N * N;
-    int64_t blocks = std::min<int64_t>(wave, (rows + kRowThreads - 1) / kRowThreads);
+    int64_t blocks = std::min<int64_t>(kUpdBlocks, (rows + kRowThreads - 1) / kRowThreads);
     if (cap > 0 && cap <= kReduceBlocksMax) blocks = std::min<int64_t>(rows, cap);
     return (unsigned)(blocks > 0 ? blocks : 1);
 }
@@ -300,197 +300,13 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     });
 }
 
-// Software-pipelined row tail (SEM_CG_UPD=2): the own w row and the r row
-// of the thread's NEXT grid-stride row are loaded before the current row is
-// assembled, so two rows' worth of loads are in flight per thread (more
-// registers: 4 blocks per SM, one wave = 4 x 148 blocks).
-#ifndef SEM_UPD4_MINB
-#define SEM_UPD4_MINB 4
-#endif
-constexpr int kUpd4MinB = SEM_UPD4_MINB;
-template <int N, bool DIST>
-__global__ void __launch_bounds__(kRowThreads, kUpd4MinB)
-cg_update4_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, Box bx,
-                  sem_cg_state* st, double* history, ReduceScratch* rs,
-                  const double* __restrict__ bot, const double* __restrict__ top)
-{
-    constexpr int NN = N * N;
-    griddep_wait();
-    if (st->stop) return;
-    const double nalpha = -st->alpha;
-    double acc = 0.0;
-    const int64_t rows = E * NN, stride = (int64_t)gridDim.x * kRowThreads;
-    int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x;
-    double wn[N], rn[N];
-    if (row < rows) {
-        load_row<N>(w + row * N, wn);
-        load_row_rw<N>(r + row * N, rn);
-    }
-    for (; row < rows; row += stride) {
-        double wc[N], rv[N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            wc[i] = wn[i];
-            rv[i] = rn[i];
-        }
-        const int64_t nx = row + stride;
-        if (nx < rows) {
-            load_row<N>(w + nx * N, wn);
-            load_row_rw<N>(r + nx * N, rn);
-        }
-        const Row<N> rw = make_row<N>(row, bx);
-        double v[N];
-        dssum_row_own<N>(w, rw, bx, DIST ? bot : nullptr, DIST ? top : nullptr, wc, v);
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            rv[i] = add_rn(rv[i], mul_rn(nalpha, mul_rn(v[i], row_mask<N>(rw, i))));
-            acc += mul_rn(mul_rn(rv[i], rv[i]), row_inv_mult<N>(rw, i));
-        }
-        store_row<N>(r + row * N, rv);
-    }
-    griddep_launch();
-    const double vals[1] = {acc};
-    reduce_publish_and_finish<1, kRowThreads>(vals, rs, [&](const double (&t)[1]) {
-        if (DIST) st->local_sum = t[0];
-        else fin_rr(st, t[0], history);
-    });
-}
-
-// Flat-pair form of the iteration tail (same arithmetic, same ordered
-// gather): thread q owns the point pair (2q, 2q+1) of one row (n even; one
-// point for odd n), so the own w / r loads and the r store are fully
-// coalesced 128-bit accesses, and every copy of the pair's points -- up to
-// 2 x 2 (z, y) copies, each with its x-neighbour scalars -- is loaded
-// up-front under predicates before any addition consumes it, so all of a
-// thread's loads are in flight at once.  The sums then run in the
-// reference's ascending-element order: (z, y) copies lexicographically,
-// within each the x-lower copy, the own-x copy, the x-upper copy.
-template <int N, bool DIST>
-__global__ void __launch_bounds__(PairCfg<N>::THREADS)
-cg_update3_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, BoxFlat bf,
-                  sem_cg_state* st, double* history, ReduceScratch* rs,
-                  const double* __restrict__ bot, const double* __restrict__ top)
-{
-    constexpr int NNN = N * N * N;
-    if (st->stop) return;
-    const double nalpha = -st->alpha;
-    const Box& b = bf.b;
-    double acc = 0.0;
-    SEM_PAIR_LOOP(E) {
-        const int64_t q0 = u_ * NP;
-        ElemCoord c;
-        int i, j, k;
-        pair_point<N>(q0, bf, c, i, j, k);
-        double rv[NP];
-        ld_pair_rw<N>(r + q0, rv);
-        const AxisCopies ay = axis_copies<N>(c.iy, j, b.ey);
-        const AxisCopies az = axis_copies<N>(c.iz, k, b.ez);
-        bool xlo[NP], xhi[NP];
-#pragma unroll
-        for (int h = 0; h < NP; ++h) {
-            xlo[h] = (i + h == 0) && c.ix > 0;
-            xhi[h] = (i + h == N - 1) && c.ix < b.ex - 1;
-        }
-        const double* plane = nullptr;
-        if (DIST) {
-            if (bot != nullptr && c.iz == 0 && k == 0) plane = bot;
-            if (top != nullptr && c.iz == b.ez - 1 && k == N - 1) plane = top;
-        }
-        // loads: copy (zc, yc) at source element e + dz*ex*ey + dy*ex
-        double s[2][2][NP], lo[2][2][NP], hi[2][2][NP];
-        const int64_t e_own = q0 / NNN;
-        const int64_t exy = (int64_t)b.ex * b.ey;
-#pragma unroll
-        for (int zc = 0; zc < 2; ++zc) {
-#pragma unroll
-            for (int yc = 0; yc < 2; ++yc) {
-                const bool ok = zc < az.cnt && yc < ay.cnt && plane == nullptr;
-                const int ez_ = zc ? az.e1 : az.e0, kk = zc ? az.l1 : az.l0;
-                const int ey_ = yc ? ay.e1 : ay.e0, jj = yc ? ay.l1 : ay.l0;
-                const int64_t e2 = e_own + (int64_t)(ez_ - c.iz) * exy + (int64_t)(ey_ - c.iy) * b.ex;
-                const double* src = w + e2 * NNN + (kk * N + jj) * N + i;
-                if (ok) {
-                    ld_pair<N>(src, s[zc][yc]);
-                } else {
-#pragma unroll
-                    for (int h = 0; h < NP; ++h) s[zc][yc][h] = 0.0;
-                }
-#pragma unroll
-                for (int h = 0; h < NP; ++h) {
-                    lo[zc][yc][h] = (ok && xlo[h]) ? __ldg(src + h - NNN + (N - 1)) : 0.0;
-                    hi[zc][yc][h] = (ok && xhi[h]) ? __ldg(src + h + NNN - (N - 1)) : 0.0;
-                }
-            }
-        }
-        double v[NP];
-        if (DIST && plane != nullptr) {
-            const int nx = b.ex * (N - 1) + 1;
-            const double* pr = plane + (int64_t)(c.iy * (N - 1) + j) * nx + c.ix * (N - 1) + i;
-#pragma unroll
-            for (int h = 0; h < NP; ++h) v[h] = __ldg(pr + h);
-        } else {
-#pragma unroll
-            for (int h = 0; h < NP; ++h) v[h] = 0.0;
-#pragma unroll
-            for (int zc = 0; zc < 2; ++zc) {
-#pragma unroll
-                for (int yc = 0; yc < 2; ++yc) {
-                    if (zc < az.cnt && yc < ay.cnt) {
-#pragma unroll
-                        for (int h = 0; h < NP; ++h) {
-                            double t = v[h];
-                            if (xlo[h]) t = add_rn(t, lo[zc][yc][h]);
-                            t = add_rn(t, s[zc][yc][h]);
-                            if (xhi[h]) t = add_rn(t, hi[zc][yc][h]);
-                            v[h] = t;
-                        }
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < NP; ++h) {
-            rv[h] = add_rn(rv[h], mul_rn(nalpha, mul_rn(v[h], mask_of<N>(c, i + h, j, k, b))));
-            acc += mul_rn(mul_rn(rv[h], rv[h]), inv_mult_of<N>(c, i + h, j, k, b));
-        }
-        st_pair<N>(r + q0, rv);
-    }
-    const double vals[1] = {acc};
-    reduce_publish_and_finish<1, PairCfg<N>::THREADS>(vals, rs, [&](const double (&t)[1]) {
-        if (DIST) st->local_sum = t[0];
-        else fin_rr(st, t[0], history);
-    });
-}
-
-// which tail kernel (tuning hook SEM_CG_UPD: 0 rows, 1 flat pairs, 2 pipelined rows)
-static int upd_kind()
-{
-    static const int k = getenv("SEM_CG_UPD") ? atoi(getenv("SEM_CG_UPD")) : 0;
-    return k;
-}
-
-template <int N>
-static unsigned upd3_grid(int64_t E)
-{
-    static const int cap = getenv("SEM_CG_UPD_BLOCKS") ? atoi(getenv("SEM_CG_UPD_BLOCKS")) : 0;
-    const int lim = (cap > 0 && cap <= kReduceBlocksMax) ? cap : kReduceBlocksMax;
-    return flat_grid<N>(E, lim);
-}
-
 template <int N, bool DIST>
 static void launch_update(const double* w, double* r, int64_t E, const Box& bx, sem_cg_state* st,
                           double* history, ReduceScratch* rs, const double* bot,
                           const double* top, cudaStream_t s)
 {
-    if (upd_kind() == 1)
-        cg_update3_kernel<N, DIST><<<upd3_grid<N>(E), PairCfg<N>::THREADS, 0, s>>>(
-            w, r, E, make_box_flat(bx), st, history, rs, bot, top);
-    else if (upd_kind() == 2)
-        cg_update4_kernel<N, DIST><<<upd_grid<N>(E, kUpd4MinB * 148), kRowThreads, 0, s>>>(
-            w, r, E, bx, st, history, rs, bot, top);
-    else
-        cg_update2_kernel<N, DIST><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, bx, st, history,
-                                                                         rs, bot, top);
+    cg_update2_kernel<N, DIST><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, bx, st, history,
+                                                                     rs, bot, top);
 }
 
 // Finish a deferred reduction of the single-GPU iteration: the fixed-order
@@ -586,8 +402,6 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
                                       (const double*)rs->partials[0], (int)ug, st, history, 0),
                              "cg settle (rr)"))
                 return rc;
-        } else if (upd_kind() != 0) {
-            launch_update<N, false>(w, r, E, bx, st, history, rs, nullptr, nullptr, s);
         } else {
             if (int rc = chk(launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
                                       dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E, bx, st,

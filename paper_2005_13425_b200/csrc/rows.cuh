@@ -155,57 +155,4 @@ __device__ __forceinline__ void dssum_row(const double* __restrict__ f, const Ro
     }
 }
 
-// dssum_row with the row's OWN copy already in registers (`own`, loaded
-// ahead by the caller): the copy (zc, yc) that is this element's own row is
-// taken from `own`, every other copy is loaded; same addition order.
-template <int N>
-__device__ __forceinline__ void dssum_row_own(const double* __restrict__ f, const Row<N>& r,
-                                              const Box& b, const double* __restrict__ bot,
-                                              const double* __restrict__ top,
-                                              const double (&own)[N], double (&v)[N])
-{
-    constexpr int NNN = N * N * N;
-    const double* plane = nullptr;
-    if (bot != nullptr && r.c.iz == 0 && r.k == 0) plane = bot;
-    if (top != nullptr && r.c.iz == b.ez - 1 && r.k == N - 1) plane = top;
-    if (plane != nullptr) {
-        const int nx = b.ex * (N - 1) + 1;
-        const double* pr = plane + (int64_t)(r.c.iy * (N - 1) + r.j) * nx + r.c.ix * (N - 1);
-#pragma unroll
-        for (int i = 0; i < N; ++i) v[i] = __ldg(pr + i);
-        return;
-    }
-    const AxisCopies ay = axis_copies<N>(r.c.iy, r.j, b.ey);
-    const AxisCopies az = axis_copies<N>(r.c.iz, r.k, b.ez);
-#pragma unroll
-    for (int i = 0; i < N; ++i) v[i] = 0.0;
-#pragma unroll
-    for (int zc = 0; zc < 2; ++zc) {
-        if (zc >= az.cnt) break;
-        const int ez_ = zc ? az.e1 : az.e0, kk = zc ? az.l1 : az.l0;
-#pragma unroll
-        for (int yc = 0; yc < 2; ++yc) {
-            if (yc >= ay.cnt) break;
-            const int ey_ = yc ? ay.e1 : ay.e0, jj = yc ? ay.l1 : ay.l0;
-            const int64_t e2 = ((int64_t)ez_ * b.ey + ey_) * b.ex + r.c.ix;
-            const double* src = f + e2 * NNN + (kk * N + jj) * N;
-            const bool is_own = ez_ == r.c.iz && ey_ == r.c.iy;
-            double s[N];
-            if (is_own) {
-#pragma unroll
-                for (int i = 0; i < N; ++i) s[i] = own[i];
-            } else {
-                load_row<N>(src, s);
-            }
-            const double lo = r.x_lo_in ? __ldg(src - NNN + (N - 1)) : 0.0;
-            const double hi = r.x_hi_in ? __ldg(src + NNN) : 0.0;
-            v[0] = r.x_lo_in ? add_rn(add_rn(v[0], lo), s[0]) : add_rn(v[0], s[0]);
-#pragma unroll
-            for (int i = 1; i < N - 1; ++i) v[i] = add_rn(v[i], s[i]);
-            v[N - 1] = r.x_hi_in ? add_rn(add_rn(v[N - 1], s[N - 1]), hi)
-                                 : add_rn(v[N - 1], s[N - 1]);
-        }
-    }
-}
-
 }  // namespace sem
