@@ -34,8 +34,13 @@ struct HalfCfg {
     static constexpr int NP = ((NN + 31) / 32) * 32;  // threads per half
     static constexpr int THREADS = 2 * NP;
     using P = PencilCfg<N>;
-    static constexpr int LSU = P::LSU, LSA = P::LSA, LSB = P::LSB;
-    static constexpr size_t SMEM = sizeof(double) * (size_t)P::SLOT_DOUBLES;
+    // unpadded rows (RS = N) and layer strides == N (mod 16).  Measured
+    // (profiles/r01_ax_row_stride.txt): the pencil kernel's padded rows
+    // (RS == 2 mod 4) cost this kernel 7-10% at n = 12, an odd stride 7-16%.
+    static constexpr int RS = N, LSA = NN;
+    static constexpr int LSB = NN + (((N - NN) % 16) + 16) % 16;
+    static constexpr int LSU = LSB;
+    static constexpr size_t SMEM = sizeof(double) * (size_t)N * (LSU + LSA + LSB);
 };
 
 // the k-direction work of one half-pencil: H = 0 (k < KH) or 1 (k >= KH)
@@ -78,7 +83,7 @@ ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
 {
     using C = HalfCfg<N>;
     constexpr int NN = C::NN, NNN = C::NNN, KH = C::KH, LSU = C::LSU, LSA = C::LSA,
-                  LSB = C::LSB, NP = C::NP;
+                  LSB = C::LSB, NP = C::NP, RS = C::RS;
     extern __shared__ __align__(16) double smem[];
     double* U = smem;             // u stack; after S1/S2 it holds ut (UT)
     double* A = U + N * LSU;
@@ -88,6 +93,7 @@ ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
     const int h = tid / NP;       // warp-uniform half
     const int q = tid - h * NP;   // k-pencil / i-pencil / j-pencil index
     const bool ok = q < NN;
+    const int kq = (q / N) * RS + q % N;  // k-pencil (i, j) = q: offset in a stack layer
     const int64_t e = blockIdx.x;
     const double* ue = u + e * NNN;
     const double* ge = g + e * 6 * NNN;
@@ -102,7 +108,7 @@ ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
     if (ok) {
 #pragma unroll
         for (int m = 0; m < KH; ++m)
-            if (m < NK) U[(K0 + m) * LSU + q] = __ldg(ue + (K0 + m) * NN + q);
+            if (m < NK) U[(K0 + m) * LSU + kq] = __ldg(ue + (K0 + m) * NN + q);
 #pragma unroll
         for (int d = 0; d < PD; ++d)
 #pragma unroll
@@ -112,29 +118,29 @@ ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
     __syncthreads();
     double wt[KH];
     if (ok) {
-        if (h == 0) half_k_stages_s3<N, 0, PD>(D, U, q, wt);
-        else half_k_stages_s3<N, 1, PD>(D, U, q, wt);
+        if (h == 0) half_k_stages_s3<N, 0, PD>(D, U, kq, wt);
+        else half_k_stages_s3<N, 1, PD>(D, U, kq, wt);
     }
     // ---- S1 (h = 0): i-pencil (j,k) = q ; S2 (h = 1): j-pencil (i,k) = q
     if (ok) {
         const int a = q % N, k = q / N;
         double in[N], out[N];
         if (h == 0) {
-            const double* src = U + k * LSU + a * N;  // row (j = a, k)
+            const double* src = U + k * LSU + a * RS;  // row (j = a, k)
 #pragma unroll
             for (int l = 0; l < N; ++l) in[l] = src[l];
             pencil_gemv<N, FOLD, false>(D, kStS1, in, out);
-            double* dst = A + k * LSA + a * N;
+            double* dst = A + k * LSA + a * RS;
 #pragma unroll
             for (int i = 0; i < N; ++i) dst[i] = out[i];
         } else {
             const double* src = U + k * LSU + a;      // column (i = a, k)
 #pragma unroll
-            for (int l = 0; l < N; ++l) in[l] = src[l * N];
+            for (int l = 0; l < N; ++l) in[l] = src[l * RS];
             pencil_gemv<N, FOLD, false>(D, kStS2, in, out);
             double* dst = B + k * LSB + a;
 #pragma unroll
-            for (int j = 0; j < N; ++j) dst[j * N] = out[j];
+            for (int j = 0; j < N; ++j) dst[j * RS] = out[j];
         }
     }
     __syncthreads();
@@ -153,25 +159,25 @@ ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
                     for (int c = 0; c < 6; ++c)
                         gq[m % PD][c] = __ldg(ge + c * NNN + (k + PD) * NN + q);
                 }
-                const double av = A[k * LSA + q], bv = B[k * LSB + q], tv = wt[m];
-                A[k * LSA + q] = fma(gc[2], tv, fma(gc[1], bv, gc[0] * av));
-                B[k * LSB + q] = fma(gc[4], tv, fma(gc[3], bv, gc[1] * av));
-                U[k * LSU + q] = fma(gc[5], tv, fma(gc[4], bv, gc[2] * av));
+                const double av = A[k * LSA + kq], bv = B[k * LSB + kq], tv = wt[m];
+                A[k * LSA + kq] = fma(gc[2], tv, fma(gc[1], bv, gc[0] * av));
+                B[k * LSB + kq] = fma(gc[4], tv, fma(gc[3], bv, gc[1] * av));
+                U[k * LSU + kq] = fma(gc[5], tv, fma(gc[4], bv, gc[2] * av));
             }
         }
     }
     __syncthreads();
     double Wt[KH];
     if (ok) {
-        if (h == 0) half_k_wt<N, 0>(D, U, q, Wt);
-        else half_k_wt<N, 1>(D, U, q, Wt);
+        if (h == 0) half_k_wt<N, 0>(D, U, kq, Wt);
+        else half_k_wt<N, 1>(D, U, kq, Wt);
     }
     // ---- S5 (h = 0): A rows <- D^T ; S6 (h = 1): B columns <- D^T
     if (ok) {
         const int a = q % N, k = q / N;
         double in[N], out[N];
         if (h == 0) {
-            double* rp = A + k * LSA + a * N;
+            double* rp = A + k * LSA + a * RS;
 #pragma unroll
             for (int l = 0; l < N; ++l) in[l] = rp[l];
             pencil_gemv<N, FOLD, true>(D, kStS5, in, out);
@@ -180,10 +186,10 @@ ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
         } else {
             double* cp = B + k * LSB + a;
 #pragma unroll
-            for (int l = 0; l < N; ++l) in[l] = cp[l * N];
+            for (int l = 0; l < N; ++l) in[l] = cp[l * RS];
             pencil_gemv<N, FOLD, true>(D, kStS6, in, out);
 #pragma unroll
-            for (int j = 0; j < N; ++j) cp[j * N] = out[j];
+            for (int j = 0; j < N; ++j) cp[j * RS] = out[j];
         }
     }
     __syncthreads();
@@ -195,7 +201,7 @@ ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
         for (int m = 0; m < KH; ++m) {
             if (m < NK) {
                 const int k = K0 + m;
-                __stcs(we + k * NN, (A[k * LSA + q] + B[k * LSB + q]) + Wt[m]);
+                __stcs(we + k * NN, (A[k * LSA + kq] + B[k * LSB + kq]) + Wt[m]);
             }
         }
     }

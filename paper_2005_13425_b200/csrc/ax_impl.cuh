@@ -372,7 +372,8 @@ template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0, in
 static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
                       cudaStream_t stream, CgpArgs cgp = CgpArgs{})
 {
-    if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 && (GMODE < 2 || N % 2 == 0) &&
+    if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 &&
+                  (GMODE < 2 || (N % 2 == 0 && PencilCfg<N>::RS == N)) &&
                   (GMODE < 3 || (SLOTS == 1 && CGM != 0)) &&
                   sizeof(double) * ((size_t)SLOTS * PencilCfg<N>::SLOT_DOUBLES +
                                     (GMODE ? (size_t)SLOTS * 6 * N * N * N + 6 : 0)) * MINB <= 227 * 1024)
@@ -427,7 +428,7 @@ static int launch_half(const double* u, const double* g, const double* dx, doubl
 // profiles/r01_ax_sweep.txt, r01_ax_sweep_self_pf_raw.jsonl, CUDA-graph
 // timed): index = n, value = variant id.  n >= 12: folded register ring with
 // the CTA's own element bulk-prefetched into L2 at start (+10..30%).
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 57, 55, 59, 54, 48};
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 57, 55, 59, 54, 47};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,

@@ -35,8 +35,13 @@ struct PencilCfg {
     static constexpr int NN = N * N;
     static constexpr int NNN = N * N * N;
     // layer strides in doubles
-    static constexpr int LSA = NN;                                  // row-friendly
-    static constexpr int LSB = NN + (((N - NN) % 16) + 16) % 16;    // == N (mod 16)
+    // row stride RS (doubles): == 2 (mod 4) for even N so the i-pencil's
+    // 128-bit row loads of consecutive threads hit distinct bank groups
+    // (N = 4, 8, 12, 16 would otherwise put every row on the same banks);
+    // odd N use scalar loads and RS = N (odd) is conflict-free
+    static constexpr int RS = (N % 2 == 1 || N % 4 == 2) ? N : N + 2;
+    static constexpr int LSA = N * RS;                              // row-friendly
+    static constexpr int LSB = N * RS + (((N - N * RS) % 16) + 16) % 16;  // == N (mod 16)
     static constexpr int LSU = LSB;
     static constexpr int SLOT_DOUBLES = N * (LSU + LSA + LSB);
     static constexpr int SLOTS = (N <= 4)  ? (512 / NN)
@@ -219,7 +224,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                  int64_t pf_elems, CgpArgs cgp)
 {
     using C = PencilCfg<N>;
-    constexpr int NN = C::NN, NNN = C::NNN, LSU = C::LSU, LSA = C::LSA, LSB = C::LSB;
+    constexpr int NN = C::NN, NNN = C::NNN, LSU = C::LSU, LSA = C::LSA, LSB = C::LSB, RS = C::RS;
     extern __shared__ __align__(16) double smem[];
 
     const int tid = threadIdx.x;
@@ -240,6 +245,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
 
     // index maps of the three pencil families (see header comment)
     const int kp_i = p % N, kp_j = p / N;          // k-pencil (i,j): p = j*N + i
+    const int kp = kp_j * RS + kp_i;               // its offset within a stack layer
     const int ip_j = p % N, ip_k = p / N;          // i-pencil (j,k): p = k*N + j
     const int jp_i = p % N, jp_k = p / N;          // j-pencil (i,k): p = k*N + i
 
@@ -356,6 +362,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             for (int k = 0; k < N; ++k) ucol[k] = ok ? __ldg(src + k * NN) : 0.0;
         }
     };
+    static_assert(GMODE < 2 || RS == N, "bulk copies into the stacks need unpadded rows");
     static_assert(GMODE < 3 || (CGM != 0 && SLOTS == 1 && N % 2 == 0),
                   "GMODE 3/4: CG fusion, one element per CTA, 16-byte layer copies");
     if constexpr (GMODE < 2) load_ucol(batch);
@@ -406,10 +413,10 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                     const int64_t off = e * NNN + p;
 #pragma unroll
                     for (int k = 0; k < N; ++k) {
-                        const double po = U[k * LSU + p];
+                        const double po = U[k * LSU + kp];
                         if (xpend)
-                            cgp.x[off + k * NN] = add_rn(B[k * LSB + p], mul_rn(alpha_prev, po));
-                        ucol[k] = add_rn(mul_rn(beta, po), A[k * LSA + p]);
+                            cgp.x[off + k * NN] = add_rn(B[k * LSB + kp], mul_rn(alpha_prev, po));
+                        ucol[k] = add_rn(mul_rn(beta, po), A[k * LSA + kp]);
                         cgp.p[off + k * NN] = ucol[k];
                     }
                 } else {
@@ -420,7 +427,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             if constexpr (GMODE == 2) {
                 mbar_wait(ubar, 0);
 #pragma unroll
-                for (int k = 0; k < N; ++k) ucol[k] = active ? U[k * LSU + p] : 0.0;
+                for (int k = 0; k < N; ++k) ucol[k] = active ? U[k * LSU + kp] : 0.0;
             }
         } else {
 #pragma unroll
@@ -448,14 +455,14 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         double wt[N];
 #pragma unroll
         for (int k = 0; k < N; ++k)
-            if (GMODE != 2 && lane_ok) U[k * LSU + p] = ucol[k];
+            if (GMODE != 2 && lane_ok) U[k * LSU + kp] = ucol[k];
         pencil_gemv<N, FOLD, false>(D, kStS3, ucol, wt);
         __syncthreads();
 
         // ---- S1: i-pencil (j,k): wr[i] = sum_l D[i][l] U[k][j][l] ----------
         if (lane_ok) {
             double row[N];
-            const double* src = U + ip_k * LSU + ip_j * N;
+            const double* src = U + ip_k * LSU + ip_j * RS;
             if (C::VEC) {
 #pragma unroll
                 for (int q = 0; q < N / 2; ++q) {
@@ -469,7 +476,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             }
             double out[N];
             pencil_gemv<N, FOLD, false>(D, kStS1, row, out);
-            double* dst = A + ip_k * LSA + ip_j * N;
+            double* dst = A + ip_k * LSA + ip_j * RS;
             if (C::VEC) {
 #pragma unroll
                 for (int q = 0; q < N / 2; ++q)
@@ -484,12 +491,12 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             double col[N];
             const double* src = U + jp_k * LSU + jp_i;
 #pragma unroll
-            for (int l = 0; l < N; ++l) col[l] = src[l * N];
+            for (int l = 0; l < N; ++l) col[l] = src[l * RS];
             double* dst = B + jp_k * LSB + jp_i;
             double out[N];
             pencil_gemv<N, FOLD, false>(D, kStS2, col, out);
 #pragma unroll
-            for (int j = 0; j < N; ++j) dst[j * N] = out[j];
+            for (int j = 0; j < N; ++j) dst[j * RS] = out[j];
         }
         __syncthreads();
 
@@ -515,14 +522,14 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                 }
             }
             if (lane_ok) {
-                const double a = A[k * LSA + p];
-                const double b = B[k * LSB + p];
+                const double a = A[k * LSA + kp];
+                const double b = B[k * LSB + kp];
                 const double t = wt[k];
                 const double ur = fma(gc[2], t, fma(gc[1], b, gc[0] * a));
                 const double us = fma(gc[4], t, fma(gc[3], b, gc[1] * a));
                 const double ut = fma(gc[5], t, fma(gc[4], b, gc[2] * a));
-                A[k * LSA + p] = ur;
-                B[k * LSB + p] = us;
+                A[k * LSA + kp] = ur;
+                B[k * LSB + kp] = us;
                 if constexpr (FOLD) {
                     utk[k] = ut;  // folded D^T applied once all layers are known
                 } else {
@@ -540,7 +547,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         // ---- S5: i-pencil: A row <- D^T A row ------------------------------
         if (lane_ok) {
             double row[N];
-            double* rp = A + ip_k * LSA + ip_j * N;
+            double* rp = A + ip_k * LSA + ip_j * RS;
             if (C::VEC) {
 #pragma unroll
                 for (int q = 0; q < N / 2; ++q) {
@@ -568,11 +575,11 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             double col[N];
             double* cp = B + jp_k * LSB + jp_i;
 #pragma unroll
-            for (int l = 0; l < N; ++l) col[l] = cp[l * N];
+            for (int l = 0; l < N; ++l) col[l] = cp[l * RS];
             double out[N];
             pencil_gemv<N, FOLD, true>(D, kStS6, col, out);
 #pragma unroll
-            for (int j = 0; j < N; ++j) cp[j * N] = out[j];
+            for (int j = 0; j < N; ++j) cp[j * RS] = out[j];
         }
         // next batch's u columns: in flight across the barrier and S7
         if (PERSIST && GMODE != 2) load_ucol(batch + gridDim.x);
@@ -583,9 +590,9 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             double* we = w + e * NNN + p;
 #pragma unroll
             for (int k = 0; k < N; ++k) {
-                const double v = (A[k * LSA + p] + B[k * LSB + p]) + Wt[k];
+                const double v = (A[k * LSA + kp] + B[k * LSB + kp]) + Wt[k];
                 __stcs(we + k * NN, v);
-                if constexpr (CGM != 0) pap_acc = fma(U[k * LSU + p], v, pap_acc);  // U = p_new
+                if constexpr (CGM != 0) pap_acc = fma(U[k * LSU + kp], v, pap_acc);  // U = p_new
             }
         }
         // (no barrier needed: the next S3 writes only U, last read before the
