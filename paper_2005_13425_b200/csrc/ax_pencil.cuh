@@ -38,12 +38,16 @@ struct PencilCfg {
     // row stride RS (doubles): == 2 (mod 4) for even N so the i-pencil's
     // 128-bit row loads of consecutive threads hit distinct bank groups
     // (N = 4, 8, 12, 16 would otherwise put every row on the same banks);
-    // odd N use scalar loads and RS = N (odd) is conflict-free
+    // odd N use scalar loads and RS = N (odd) is conflict-free (padding odd
+    // rows to 128-bit accesses measured 6% slower at n = 13, 15:
+    // profiles/r01_ax_row_stride.txt)
+    static constexpr bool VECROW = (N % 2 == 0);
     static constexpr int RS = (N % 2 == 1 || N % 4 == 2) ? N : N + 2;
     static constexpr int LSA = N * RS;                              // row-friendly
     static constexpr int LSB = N * RS + (((N - N * RS) % 16) + 16) % 16;  // == N (mod 16)
-    static constexpr int LSU = LSB;
-    static constexpr int SLOT_DOUBLES = N * (LSU + LSA + LSB);
+    // U is read by 128-bit rows too: keep its layers 16-byte aligned
+    static constexpr int LSU = (VECROW && LSB % 2) ? LSB + 1 : LSB;
+    static constexpr int SLOT_DOUBLES = (N * (LSU + LSA + LSB) + 1) / 2 * 2;
     static constexpr int SLOTS = (N <= 4)  ? (512 / NN)
                                : (N <= 6)  ? (576 / NN)
                                : (N <= 8)  ? 8
@@ -56,6 +60,38 @@ struct PencilCfg {
     static constexpr size_t SMEM = sizeof(double) * (size_t)SLOTS * SLOT_DOUBLES;
     static constexpr bool VEC = (N % 2) == 0;
 };
+
+// One stack row (N doubles at a 16-byte-aligned row start) to / from
+// registers: 128-bit accesses when the row stride allows them (the pad
+// double of an odd row is read and ignored / written as 0).
+template <int N>
+__device__ __forceinline__ void stack_row_ld(const double* src, double (&v)[N])
+{
+    if constexpr (PencilCfg<N>::VECROW) {
+#pragma unroll
+        for (int q = 0; q < (N + 1) / 2; ++q) {
+            const double2 t = reinterpret_cast<const double2*>(src)[q];
+            v[2 * q] = t.x;
+            if (2 * q + 1 < N) v[2 * q + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int l = 0; l < N; ++l) v[l] = src[l];
+    }
+}
+template <int N>
+__device__ __forceinline__ void stack_row_st(double* dst, const double (&v)[N])
+{
+    if constexpr (PencilCfg<N>::VECROW) {
+#pragma unroll
+        for (int q = 0; q < (N + 1) / 2; ++q)
+            reinterpret_cast<double2*>(dst)[q] =
+                make_double2(v[2 * q], 2 * q + 1 < N ? v[2 * q + 1] : 0.0);
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) dst[i] = v[i];
+    }
+}
 
 // One private copy of D per contraction stage: with a single copy the
 // compiler common-subexpressions the constant loads across stages and keeps
@@ -462,29 +498,10 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         // ---- S1: i-pencil (j,k): wr[i] = sum_l D[i][l] U[k][j][l] ----------
         if (lane_ok) {
             double row[N];
-            const double* src = U + ip_k * LSU + ip_j * RS;
-            if (C::VEC) {
-#pragma unroll
-                for (int q = 0; q < N / 2; ++q) {
-                    const double2 v = reinterpret_cast<const double2*>(src)[q];
-                    row[2 * q] = v.x;
-                    row[2 * q + 1] = v.y;
-                }
-            } else {
-#pragma unroll
-                for (int l = 0; l < N; ++l) row[l] = src[l];
-            }
+            stack_row_ld<N>(U + ip_k * LSU + ip_j * RS, row);
             double out[N];
             pencil_gemv<N, FOLD, false>(D, kStS1, row, out);
-            double* dst = A + ip_k * LSA + ip_j * RS;
-            if (C::VEC) {
-#pragma unroll
-                for (int q = 0; q < N / 2; ++q)
-                    reinterpret_cast<double2*>(dst)[q] = make_double2(out[2 * q], out[2 * q + 1]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < N; ++i) dst[i] = out[i];
-            }
+            stack_row_st<N>(A + ip_k * LSA + ip_j * RS, out);
         }
         // ---- S2: j-pencil (i,k): ws[j] = sum_l D[j][l] U[k][l][i] ----------
         if (lane_ok) {
@@ -548,27 +565,10 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         if (lane_ok) {
             double row[N];
             double* rp = A + ip_k * LSA + ip_j * RS;
-            if (C::VEC) {
-#pragma unroll
-                for (int q = 0; q < N / 2; ++q) {
-                    const double2 v = reinterpret_cast<const double2*>(rp)[q];
-                    row[2 * q] = v.x;
-                    row[2 * q + 1] = v.y;
-                }
-            } else {
-#pragma unroll
-                for (int l = 0; l < N; ++l) row[l] = rp[l];
-            }
+            stack_row_ld<N>(rp, row);
             double out[N];
             pencil_gemv<N, FOLD, true>(D, kStS5, row, out);
-            if (C::VEC) {
-#pragma unroll
-                for (int q = 0; q < N / 2; ++q)
-                    reinterpret_cast<double2*>(rp)[q] = make_double2(out[2 * q], out[2 * q + 1]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < N; ++i) rp[i] = out[i];
-            }
+            stack_row_st<N>(rp, out);
         }
         // ---- S6: j-pencil: B col <- D^T B col ------------------------------
         if (lane_ok) {
