@@ -19,9 +19,10 @@ def main(path, title):
     tot = sum(sum(v) for v in agg.values())
     print(f"# {title}")
     print("# gpu__time_duration.sum, --clock-control none: cold-cache serialised launches, compare SHARES")
-    print(f"{'kernel':80s} {'launches':>8s} {'mean_us':>9s} {'share':>7s}")
+    print(f"{'kernel':80s} {'launches':>8s} {'mean_us':>9s} {'median_us':>9s} {'share':>7s}")
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-        print(f"{k:80s} {len(v):8d} {sum(v) / len(v):9.2f} {sum(v) / tot:7.1%}")
+        med = sorted(v)[len(v) // 2]
+        print(f"{k:80s} {len(v):8d} {sum(v) / len(v):9.2f} {med:9.2f} {sum(v) / tot:7.1%}")
 
 
 if __name__ == "__main__":
