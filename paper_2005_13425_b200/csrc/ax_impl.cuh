@@ -374,7 +374,7 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 {
     if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 &&
                   (GMODE < 2 || (N % 2 == 0 && PencilCfg<N>::RS == N)) &&
-                  (GMODE < 3 || (SLOTS == 1 && CGM != 0)) &&
+                  (GMODE < 4 || (SLOTS == 1 && CGM != 0)) &&
                   sizeof(double) * ((size_t)SLOTS * PencilCfg<N>::SLOT_DOUBLES +
                                     (GMODE ? (size_t)SLOTS * 6 * N * N * N + 6 : 0)) * MINB <= 227 * 1024)
         return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGM>(u, g, dx, w, E,
@@ -527,11 +527,6 @@ static int ax_cg_n(const double* g, const double* dx, double* w, int64_t E, CgpA
             case 3: return try_pencil<N, 2, 2, false, 1, false, 0, true, CGM>(p, g, dx, w, E, s, a);
             case 4: return try_pencil<N, 1, 3, false, 1, false, 1, true, CGM>(p, g, dx, w, E, s, a);
             case 5: return try_pencil<N, 1, 2, false, 1, false, 1, true, CGM>(p, g, dx, w, E, s, a);
-            // GMODE 3: p, r, x staged by bulk copies too (every load of the
-            // CTA in flight at its start), with / without the L2 prefetch
-            case 6: return try_pencil<N, 1, 3, false, 1, true, 3, true, CGM>(p, g, dx, w, E, s, a);
-            case 7: return try_pencil<N, 1, 3, false, 1, false, 3, true, CGM>(p, g, dx, w, E, s, a);
-            case 8: return try_pencil<N, 1, 2, false, 1, true, 3, true, CGM>(p, g, dx, w, E, s, a);
             // GMODE 4: all bulk copies issued before the CG scalars are read
             case 9: return try_pencil<N, 1, 3, false, 1, true, 4, true, CGM>(p, g, dx, w, E, s, a);
             case 10: return try_pencil<N, 1, 3, false, 1, false, 4, true, CGM>(p, g, dx, w, E, s, a);
@@ -544,10 +539,10 @@ static int ax_cg_n(const double* g, const double* dx, double* w, int64_t E, CgpA
     // ahead cut the fused Ax from 88 to 79 us at E = 4096 and from 608 to
     // 502 us at E = 32768 (tools/cg_tune.sh, profiles/r01_cg_tune.txt)
     //
-    // even n = 6..10: p, r and x are bulk-copied too, and every copy is issued
-    // before the CG scalars are read (GMODE 4; tools/cg_tune5.sh: E = 4096
-    // 77.2 -> 73.0 us, E = 32768 457 -> 451 us)
-    if constexpr (N >= 6 && N <= 10 && N % 2 == 0)
+    // n = 6, 10 (even, unpadded stack rows): p, r and x are bulk-copied too,
+    // and every copy is issued before the CG scalars are read (GMODE 4;
+    // tools/cg_tune5.sh: E = 4096 77.2 -> 73.0 us, E = 32768 457 -> 451 us)
+    if constexpr (N >= 6 && N <= 10 && N % 2 == 0 && PencilCfg<N>::RS == N)
         return try_pencil<N, 1, 3, false, 1, true, 4, true, CGM>(p, g, dx, w, E, s, a);
     else if constexpr (N >= 5 && N <= 11)
         return try_pencil<N, 1, 3, false, 1, true, 1, true, CGM>(p, g, dx, w, E, s, a);

@@ -329,7 +329,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         }
     };
     if constexpr (CGM != 0) {
-        static_assert(!PERSIST && GMODE != 2, "CG fusion: one batch per CTA, p via registers or GMODE 3");
+        static_assert(!PERSIST && GMODE != 2, "CG fusion: one batch per CTA, p via registers or GMODE 4");
         sem_cg_state* st = cgp.st;
         if (st->stop) {                             // uniform over the grid
             drain();
@@ -399,8 +399,9 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         }
     };
     static_assert(GMODE < 2 || RS == N, "bulk copies into the stacks need unpadded rows");
-    static_assert(GMODE < 3 || (CGM != 0 && SLOTS == 1 && N % 2 == 0),
-                  "GMODE 3/4: CG fusion, one element per CTA, 16-byte layer copies");
+    static_assert(GMODE != 3, "GMODE 3 (in-loop CG staging) was superseded by GMODE 4");
+    static_assert(GMODE < 4 || (CGM != 0 && SLOTS == 1 && N % 2 == 0),
+                  "GMODE 4: CG fusion, one element per CTA, 16-byte layer copies");
     if constexpr (GMODE < 2) load_ucol(batch);
 
     for (; batch < nbatches; batch += (PERSIST ? gridDim.x : nbatches)) {
@@ -425,23 +426,12 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                             bulk_g2s(smem + (size_t)s2 * C::SLOT_DOUBLES + k * LSU,
                                      u + (e0 + s2) * NNN + k * NN, NN * 8, ubar);
                 }
-                if constexpr (GMODE == 3) {
-                    // CG operands first (needed at once), the metric after
-                    // (needed at S4): p_old -> U layers, r -> A, x -> B layers
-                    mbar_expect_tx(ubar, (unsigned)((xpend ? 3 : 2) * NNN * 8));
-                    for (int k = 0; k < N; ++k)
-                        bulk_g2s(U + k * LSU, cgp.p + e0 * NNN + k * NN, NN * 8, ubar);
-                    bulk_g2s(A, cgp.r + e0 * NNN, NNN * 8, ubar);
-                    if (xpend)
-                        for (int k = 0; k < N; ++k)
-                            bulk_g2s(B + k * LSB, cgp.x + e0 * NNN + k * NN, NN * 8, ubar);
-                }
                 mbar_expect_tx(gbar, (unsigned)(nact * 6 * NNN * 8));
                 for (int s2 = 0; s2 < nact; ++s2)
                     bulk_g2s(Gbase + (size_t)s2 * 6 * NNN, g + (e0 + s2) * (6 * NNN),
                              6 * NNN * 8, gbar);
             }
-            if constexpr (GMODE >= 3) {
+            if constexpr (GMODE == 4) {
                 // iteration head from the staged operands (same arithmetic as
                 // load_ucol): x += alpha_prev p_old, p = beta p_old + r
                 mbar_wait(ubar, 0);
