@@ -544,6 +544,11 @@ static int ax_cg_n(const double* g, const double* dx, double* w, int64_t E, CgpA
     // tools/cg_tune5.sh: E = 4096 77.2 -> 73.0 us, E = 32768 457 -> 451 us)
     if constexpr (N >= 6 && N <= 10 && N % 2 == 0 && PencilCfg<N>::RS == N)
         return try_pencil<N, 1, 3, false, 1, true, 4, true, CGM>(p, g, dx, w, E, s, a);
+    else if constexpr (N == 11)  // 96 KB of shared memory per CTA: two per SM
+        // (three did not fit and fell back to the generic tiling: 184 -> 140 us
+        // per CG iteration at E = 4096; other n measured flat in the CTAs per
+        // SM, profiles/r01_cg_minb.txt)
+        return try_pencil<N, 1, 2, false, 1, true, 1, true, CGM>(p, g, dx, w, E, s, a);
     else if constexpr (N >= 5 && N <= 11)
         return try_pencil<N, 1, 3, false, 1, true, 1, true, CGM>(p, g, dx, w, E, s, a);
     else if constexpr (N == 4)
