@@ -52,6 +52,10 @@ const char *sem_last_error(void);
 /* Supported points per dimension n (sembench/basis.py:17-18: 2..16). */
 int sem_min_points(void);
 int sem_max_points(void);
+/* Number of launches since load whose requested kernel tiling did not fit
+ * (shared memory / threads) and ran the generic tiling instead; the tuned
+ * defaults never do (tests/test_gpu_parity.py).  Diagnostic only. */
+int64_t sem_fallback_count(void);
 
 /* ---------------------------------------------------------------- Ax ---- */
 /* w[e] = A_local u[e] for every element (kernels.py:413-468).

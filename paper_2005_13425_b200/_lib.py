@@ -50,6 +50,7 @@ SIGNATURES = {
     "sem_abi_version": (ctypes.c_int, []),
     "sem_last_error": (ctypes.c_char_p, []),
     "sem_min_points": (ctypes.c_int, []),
+    "sem_fallback_count": (ctypes.c_int64, []),
     "sem_max_points": (ctypes.c_int, []),
     "sem_ax": (ctypes.c_int, [_vp, _vp, _dp, _dp, _vp, _i64, _i32, _vp]),
     "sem_ax_variant": (ctypes.c_int, [_vp, _vp, _dp, _dp, _vp, _i64, _i32, _i32, _vp]),

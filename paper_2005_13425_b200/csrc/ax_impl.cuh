@@ -379,9 +379,11 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
                                     (GMODE ? (size_t)SLOTS * 6 * N * N * N + 6 : 0)) * MINB <= 227 * 1024)
         return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGM>(u, g, dx, w, E,
                                                                                stream, cgp);
-    else
+    else {
+        note_fallback();
         return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, CGM>(
             u, g, dx, w, E, stream, cgp);
+    }
 }
 
 // Half-pencil kernel (ax_half.cuh): two threads per k-pencil, large n.
@@ -391,6 +393,7 @@ static int launch_half(const double* u, const double* g, const double* dx, doubl
 {
     using C = HalfCfg<N>;
     if constexpr (C::THREADS > 1024 || C::SMEM * MINB > 227 * 1024) {
+        note_fallback();
         return try_pencil<N, 1, 2, false, 2, 2, 0, true>(u, g, dx, w, E, stream);
     } else {
         DParamP<N> D;

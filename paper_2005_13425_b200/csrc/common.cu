@@ -2,11 +2,16 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "sem_common.cuh"
 
 namespace sem {
 
 static thread_local char g_last_error[512] = "";
+static std::atomic<long long> g_fallbacks{0};
+
+void note_fallback() { g_fallbacks.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...)
 {
@@ -70,4 +75,6 @@ int sm_count()
 extern "C" int sem_abi_version(void) { return SEM_ABI_VERSION; }
 extern "C" const char* sem_last_error(void) { return sem::g_last_error; }
 extern "C" int sem_min_points(void) { return 2; }
+
+extern "C" int64_t sem_fallback_count(void) { return (int64_t)sem::g_fallbacks.load(); }
 extern "C" int sem_max_points(void) { return 16; }

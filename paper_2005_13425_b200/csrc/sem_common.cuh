@@ -20,6 +20,11 @@ int fail_cuda(cudaError_t err, const char* what);
 // separate from torch's).
 int bind_stream_device(cudaStream_t stream);
 
+// a requested kernel tiling that does not fit (shared memory / threads) ran
+// the generic fallback instead -- counted, so tests can assert the tuned
+// defaults never take it (sem_fallback_count)
+void note_fallback();
+
 constexpr int kNumSMsB200 = 148;
 int sm_count();
 

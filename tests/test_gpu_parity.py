@@ -449,3 +449,24 @@ def test_cg_breakdown(cuda):
         sb.cg_solve(f, sb.GlobalOperator(neg, b, topo), topo, sb.CgConfig(10, 0.0))
     with pytest.raises(sb.CgBreakdownError):
         sb.cg_solve(f, lambda p: sb.apply_global(p, neg, b, topo), topo, sb.CgConfig(10, 0.0))
+
+
+# ------------------------------------------------------------- no fallback --
+
+def test_defaults_never_take_the_generic_fallback(cuda):
+    """Every n's tuned Ax default and fused-CG tiling fits (shared memory /
+    threads); a tiling that does not fit silently runs the slow generic
+    kernel, which sem_fallback_count() exposes."""
+    from paper_2005_13425_b200._lib import load
+    lib = load()
+    before = lib.sem_fallback_count()
+    for n in range(2, 17):
+        b = sb.build_basis(n)
+        u, g = _rand_inputs(8, n, 3, 4)
+        sb.apply_ax(torch.from_numpy(u).cuda(), sb.GeomFactors(values=torch.from_numpy(g).cuda()), b)
+        mesh = sb.build_mesh(2, 2, 2, n, 1.0)
+        topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b)
+        f = sb.make_rhs(8, n, topo, sb.mix64(1, 8))
+        sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(2, 0.0))
+        torch.cuda.synchronize()
+        assert lib.sem_fallback_count() == before, f"n={n}: a default tiling fell back"
