@@ -10,7 +10,7 @@ import paper_2005_13425_b200 as sb  # noqa: E402
 from paper_2005_13425_b200.kernels import apply_ax_into  # noqa: E402
 
 dev = torch.device("cuda", 0)
-for n in (3, 4, 7, 10, 12, 16):
+for n in (3, 4, 6, 7, 8, 10, 11, 12, 14, 16):
     E = 5
     b = sb.build_basis(n)
     u = sb.random_field(E, n, 1, device=dev)
