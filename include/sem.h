@@ -154,8 +154,9 @@ int sem_cg_init(const double *f, double *x, double *r, double *p, sem_cg_state *
                 int32_t ex, int32_t ey, int32_t ez, int32_t n, void *scratch,
                 sem_stream_t stream);
 /* Enqueue `iterations` fused CG iterations on the box operator (single GPU):
- * two launches per iteration (Ax with the iteration head, x update and
- * <p,Ap> fused; r update with dssum + mask fused).  w is a 2*E*n^3 scratch
+ * per iteration the Ax kernel with the iteration head, x update and the
+ * <p,Ap> block partials fused, a one-block settle (alpha), and the r update
+ * with dssum + mask and <r,r>_c fused.  w is a 2*E*n^3 scratch
  * buffer; history receives sqrt(<r,r>_c) per iteration.  The x update of
  * the LAST iteration run is deferred: call sem_cg_finalize before reading x. */
 int sem_cg_run(const double *g, const double *dx, const double *dxt, double *x,
@@ -168,7 +169,7 @@ int sem_cg_finalize(double *x, const double *p, sem_cg_state *state, int64_t num
                     sem_stream_t stream);
 /* sem_cg_run with CUDA events between its launches (measurement only):
  * synchronises, then ADDS each phase's device milliseconds to phase_ms[0]
- * (Ax with the fused iteration head and <p,Ap>), [1] (r update with the
+ * (Ax with the fused iteration head and <p,Ap>, plus the settle), [1] (r update with the
  * fused dssum + mask, <r,r>), [2] (unused). */
 int sem_cg_run_phases(const double *g, const double *dx, const double *dxt, double *x,
                       double *r, double *p, double *w, sem_cg_state *state, double *history,
