@@ -213,9 +213,13 @@ int sem_cg_init_slab(const double *f, double *x, double *r, double *p, sem_cg_st
  * iteration): sem_cg_ax_slab on element ranges of the slab (edge layers
  * first, then the interior overlapping the halo exchange) = exact-zero exit,
  * beta, x += alpha_prev p_old (deferred), p = beta*p + r, w = A_local p and
- * this range's sum of p*(A_local p) added to (accumulate != 0) or stored in
- * state->local_sum -- gather + sem_cg_finish(phase 1) then settles alpha.
- * `partials` holds one double per element of the range (device scratch).
+ * this range's sum of p*(A_local p) added to (accumulate > 0) or stored in
+ * (accumulate == 0) state->local_sum -- gather + sem_cg_finish(phase 1) then
+ * settles alpha.  `partials` holds one double per element of the range
+ * (device scratch).  accumulate < 0 only leaves the per-element-slot partials
+ * there; one sem_cg_settle_slab over the slots of all of an iteration's
+ * ranges then sets local_sum (one settle per iteration instead of one per
+ * range).
  * sem_cg_update_slab = r += (-alpha) mask(dssum(w)) with the interface faces
  * from the halo totals, and this rank's <r,r>_c partial in local_sum
  * (phase 2).  sem_cg_finalize applies the last owed x update. */
@@ -223,6 +227,8 @@ int sem_cg_ax_slab(double *p, const double *r, double *x, const double *g, const
                    const double *dxt, double *w, int64_t num_elements, int32_t n,
                    sem_cg_state *state, double *history, double *partials, void *scratch,
                    int32_t accumulate, sem_stream_t stream);
+int sem_cg_settle_slab(const double *partials, int64_t count, sem_cg_state *state,
+                       int32_t accumulate, sem_stream_t stream);
 int sem_cg_update_slab(const double *w, double *r, const double *bottom_totals,
                        const double *top_totals, sem_cg_state *state, int32_t ex, int32_t ey,
                        int32_t ez, int32_t n, int32_t gz0, int32_t ez_global, void *scratch,

@@ -85,6 +85,7 @@ SIGNATURES = {
                                         _i32, _i32, _i32, _i32, _vp, _vp]),
     "sem_cg_ax_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _dp, _dp, _vp, _i64, _i32, _vp, _vp,
                                       _vp, _vp, _i32, _vp]),
+    "sem_cg_settle_slab": (ctypes.c_int, [_vp, _i64, _vp, _i32, _vp]),
     "sem_cg_update_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                                           _i32, _vp, _vp]),
     "sem_cg_finish": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),

@@ -665,13 +665,39 @@ extern "C" int sem_cg_ax_slab(double* p, const double* r, double* x, const doubl
     auto* rs = static_cast<ReduceScratch*>(scratch);
     // deferred <p, A p> partial: the CTAs only publish, one settle block sums
     unsigned grid = 0;
-    const CgpArgs a{p, r, state, history, x, partials, &rs->counter, accumulate ? 1 : 0, 1,
+    const CgpArgs a{p, r, state, history, x, partials, &rs->counter, accumulate > 0 ? 1 : 0, 1,
                     &grid, 0};
     if (num_elements == 0) return 0;
     if (int rc = ax_cg_dispatch(g, dx, w, num_elements, n, a, 3, s)) return rc;
+    if (accumulate < 0) {
+        // the caller settles later (sem_cg_settle_slab) over one slot per
+        // element: slots past this launch's grid (several elements per CTA)
+        // are zeroed so the later sum sees exactly this range's partials
+        if ((int64_t)grid < num_elements) {
+            cudaError_t e = cudaMemsetAsync(partials + grid, 0,
+                                            sizeof(double) * (size_t)(num_elements - grid), s);
+            if (e != cudaSuccess) return fail_cuda(e, "sem_cg_ax_slab: pad partials");
+        }
+        return 0;
+    }
     cg_settle_kernel<kPhaseLocal><<<1, kSettleThreads, 0, s>>>(partials, (int)grid, state, history,
                                                                accumulate ? 1 : 0);
     SEM_CHECK_LAUNCH("sem_cg_ax_slab settle");
+    return 0;
+}
+
+extern "C" int sem_cg_settle_slab(const double* partials, int64_t count, sem_cg_state* state,
+                                  int32_t accumulate, sem_stream_t stream)
+{
+    if (!partials || !state || count < 0 || count > 0x7fffffffLL) {
+        set_error("sem_cg_settle_slab: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    cg_settle_kernel<kPhaseLocal><<<1, kSettleThreads, 0, s>>>(partials, (int)count, state, nullptr,
+                                                               accumulate ? 1 : 0);
+    SEM_CHECK_LAUNCH("sem_cg_settle_slab");
     return 0;
 }
 

@@ -206,6 +206,19 @@ class CudaSlabOps:
         self.dxt = np.ascontiguousarray(basis.diff_t, dtype=np.float64)
         self.lib = load()
         self._local = self.state.view(torch.float64)[9:10]  # sem_cg_state.local_sum
+        # per-iteration calls with their ctypes arguments converted once (the
+        # driver loop is host-bound at small slabs: ~12 calls per iteration)
+        self._bound: dict = {}
+
+    def _invoke(self, key, build, what: str) -> None:
+        """Call a libsem entry with memoised arguments: `build()` returns
+        (fn, args) once per (key, stream)."""
+        s = torch.cuda.current_stream(self.dev).cuda_stream
+        ent = self._bound.get((key, s))
+        if ent is None:
+            ent = build()
+            self._bound[(key, s)] = ent
+        check(ent[0](*ent[1]), what)
 
     # geometry of this slab as the C-ABI expects it
     def _slab(self):
@@ -225,37 +238,50 @@ class CudaSlabOps:
         return self._local
 
     def finish(self, phase: int, gathered: torch.Tensor) -> None:
-        check(self.lib.sem_cg_finish(dv.ptr(self.state), dv.ptr(gathered), gathered.numel(),
-                                     phase, dv.ptr(self.history), self._s()), "dist cg finish")
+        self._invoke(("finish", phase, gathered.data_ptr(), gathered.numel()), lambda: (
+            self.lib.sem_cg_finish, (dv.ptr(self.state), dv.ptr(gathered), gathered.numel(),
+                                     phase, dv.ptr(self.history), self._s())), "dist cg finish")
 
     def ax_layers(self, l0: int, l1: int, first: bool) -> None:
-        """Iteration head + w = A_local p + <p, A p> partial on element layers
-        [l0, l1) (`first`: the iteration's first range resets the partial)."""
+        """Iteration head + w = A_local p on element layers [l0, l1), leaving
+        the per-element <p, A p> partials in their slots of w2 (`first` is
+        the iteration's first range; settle() then sums every slot)."""
         p = self.part
         if l1 <= l0:
             return
-        per = p.ex * p.ey
-        e0, ne = l0 * per, (l1 - l0) * per
-        off = lambda t, width: ctypes.c_void_p(t.data_ptr() + e0 * width * 8)  # noqa: E731
-        nnn = p.n ** 3
-        check(self.lib.sem_cg_ax_slab(off(self.p, nnn), off(self.r, nnn), off(self.x, nnn),
-                                      off(self.g, 6 * nnn), dv.host_f64_ptr(self.dx),
-                                      dv.host_f64_ptr(self.dxt), off(self.w, nnn), ne, p.n,
-                                      dv.ptr(self.state), dv.ptr(self.history),
-                                      dv.ptr(self.w2), dv.ptr(self.scratch), 0 if first else 1,
-                                      self._s()), "dist cg ax")
+
+        def build():
+            per = p.ex * p.ey
+            e0, ne = l0 * per, (l1 - l0) * per
+            off = lambda t, width: ctypes.c_void_p(t.data_ptr() + e0 * width * 8)  # noqa: E731
+            nnn = p.n ** 3
+            return self.lib.sem_cg_ax_slab, (
+                off(self.p, nnn), off(self.r, nnn), off(self.x, nnn), off(self.g, 6 * nnn),
+                dv.host_f64_ptr(self.dx), dv.host_f64_ptr(self.dxt), off(self.w, nnn), ne, p.n,
+                dv.ptr(self.state), dv.ptr(self.history), off(self.w2, 1),
+                dv.ptr(self.scratch), -1, self._s())
+        self._invoke(("ax", l0, l1, bool(first)), build, "dist cg ax")
+
+    def settle(self) -> None:
+        """local_sum = the fixed-order sum of every element slot's <p, A p>
+        partial (all of this iteration's ax_layers ranges)."""
+        self._invoke(("settle",), lambda: (
+            self.lib.sem_cg_settle_slab, (dv.ptr(self.w2), self.part.num_elements,
+                                          dv.ptr(self.state), 0, self._s())), "dist cg settle")
 
     def plane_top(self, field: torch.Tensor) -> torch.Tensor:
         p = self.part
-        check(self.lib.sem_slab_plane_top(dv.ptr(field), dv.ptr(self.top_partial), p.ex, p.ey,
-                                          p.ez, p.n, self._s()), "plane top")
+        self._invoke(("top", field.data_ptr()), lambda: (
+            self.lib.sem_slab_plane_top, (dv.ptr(field), dv.ptr(self.top_partial), p.ex, p.ey,
+                                          p.ez, p.n, self._s())), "plane top")
         return self.top_partial
 
     def plane_bottom(self, field: torch.Tensor, prefix) -> torch.Tensor:
         p = self.part
-        check(self.lib.sem_slab_plane_bottom(dv.ptr(field), dv.ptr(prefix),
+        self._invoke(("bottom", field.data_ptr(), prefix.data_ptr()), lambda: (
+            self.lib.sem_slab_plane_bottom, (dv.ptr(field), dv.ptr(prefix),
                                              dv.ptr(self.bottom_totals), p.ex, p.ey, p.ez, p.n,
-                                             self._s()), "plane bottom")
+                                             self._s())), "plane bottom")
         return self.bottom_totals
 
     def dssum(self, field: torch.Tensor, bottom_totals, top_totals, apply_mask: bool = False):
@@ -271,9 +297,12 @@ class CudaSlabOps:
     def update(self, bottom_totals, top_totals) -> None:
         """r -= alpha mask(dssum(w)) (faces from the halo totals); <r,r>_c partial."""
         ptr = lambda t: dv.ptr(t) if t is not None else ctypes.c_void_p(0)  # noqa: E731
-        check(self.lib.sem_cg_update_slab(dv.ptr(self.w), dv.ptr(self.r), ptr(bottom_totals),
+        key = ("update", None if bottom_totals is None else bottom_totals.data_ptr(),
+               None if top_totals is None else top_totals.data_ptr())
+        self._invoke(key, lambda: (
+            self.lib.sem_cg_update_slab, (dv.ptr(self.w), dv.ptr(self.r), ptr(bottom_totals),
                                           ptr(top_totals), dv.ptr(self.state), *self._slab(),
-                                          dv.ptr(self.scratch), self._s()), "dist update")
+                                          dv.ptr(self.scratch), self._s())), "dist update")
 
     def finalize(self) -> None:
         """The owed x += alpha p of the last iteration run."""
@@ -338,6 +367,7 @@ def dist_cg_solve(ops, comm: SlabComm, f_local, max_iterations: int, tolerance: 
         bot, top = halo_exchange(ops, comm, ops.w,
                                  overlap=lambda: ops.ax_layers(1, ez - 1, first=False)
                                  if ez > 2 else None)
+        ops.settle()
         ops.finish(1, comm.allgather(ops.local_sum(), gathered))
         ops.update(bot, top)
         ops.finish(2, comm.allgather(ops.local_sum(), gathered))

@@ -96,6 +96,9 @@ class NumpySlabOps:
             if st["tol"] > 0.0 and rn < st["tol"]:
                 st["stop"] = 3
 
+    def settle(self):
+        """Mirror of sem_cg_settle_slab: ax_layers already accumulated."""
+
     def ax_layers(self, l0, l1, first):
         """Mirror of sem_cg_ax_slab: owed x update, p = beta p + r, w = A_local p
         and the local sum of p.(A_local p) on element layers [l0, l1)."""
