@@ -310,24 +310,24 @@ static bool fill_dparam(DParamP<N>& P, const double* dx)
 }
 
 template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0, int GMODE = 0,
-          bool FOLD = false, int CGM = 0>
+          bool FOLD = false, int CGM = 0, bool ALIAS = false>
 static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
                          int64_t E, cudaStream_t stream, CgpArgs cgp = CgpArgs{})
 {
     using C = PencilCfg<N>;
     constexpr int THREADS = ((SLOTS * C::NN + 31) / 32) * 32;
-    constexpr size_t SMEM = sizeof(double) * ((size_t)SLOTS * C::SLOT_DOUBLES +
+    constexpr size_t SMEM = sizeof(double) * ((size_t)SLOTS * slot_doubles<N, ALIAS>() +
                                               (GMODE ? (size_t)SLOTS * 6 * C::NNN + 6 : 0));
     static_assert(SMEM * MINB <= 227 * 1024, "pencil kernel shared memory");
     DParamP<N> D;
     const bool antisym = fill_dparam<N>(D, dx);
     if constexpr (FOLD) {
         if (!antisym)  // the even-odd form needs a centro-antisymmetric D
-            return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, false, CGM>(
+            return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, false, CGM, ALIAS>(
                 u, g, dx, w, E, stream, cgp);
     }
     if (E == 0) return 0;
-    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGM>;
+    auto kern = ax_pencil_kernel<N, SLOTS, THREADS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGM, ALIAS>;
     // function attributes live in each device's context: configure once per
     // (template instance, device); a benign race only repeats the setting
     static std::atomic<uint64_t> configured{0};
@@ -368,17 +368,18 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
 }
 
 template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0, int GMODE = 0,
-          bool FOLD = false, int CGM = 0>
+          bool FOLD = false, int CGM = 0, bool ALIAS = false>
 static int try_pencil(const double* u, const double* g, const double* dx, double* w, int64_t E,
                       cudaStream_t stream, CgpArgs cgp = CgpArgs{})
 {
     if constexpr (SLOTS >= 1 && SLOTS * N * N <= 1024 &&
                   (GMODE < 2 || (N % 2 == 0 && PencilCfg<N>::RS == N)) &&
                   (GMODE < 4 || (SLOTS == 1 && CGM != 0)) &&
-                  sizeof(double) * ((size_t)SLOTS * PencilCfg<N>::SLOT_DOUBLES +
+                  (!ALIAS || (!PERSIST && CGM == 0 && GMODE < 2)) &&
+                  sizeof(double) * ((size_t)SLOTS * slot_doubles<N, ALIAS>() +
                                     (GMODE ? (size_t)SLOTS * 6 * N * N * N + 6 : 0)) * MINB <= 227 * 1024)
-        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGM>(u, g, dx, w, E,
-                                                                               stream, cgp);
+        return launch_pencil<N, SLOTS, MINB, PERSIST, PD, L2PF, GMODE, FOLD, CGM, ALIAS>(
+            u, g, dx, w, E, stream, cgp);
     else {
         note_fallback();
         return launch_pencil<N, PencilCfg<N>::SLOTS, 1, false, 1, false, 0, false, CGM>(
@@ -430,8 +431,10 @@ static int launch_half(const double* u, const double* g, const double* dx, doubl
 // Default tuning point per n (tools/ax_sweep.py on B200, E=4096; see
 // profiles/r01_ax_sweep.txt, r01_ax_sweep_self_pf_raw.jsonl, CUDA-graph
 // timed): index = n, value = variant id.  n >= 12: folded register ring with
-// the CTA's own element bulk-prefetched into L2 at start (+10..30%).
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 57, 55, 59, 54, 47};
+// the CTA's own element bulk-prefetched into L2 at start (+10..30%); n = 15,
+// 16 with the B stack aliasing U (profiles/r01_ax_row_stride.txt: 171 -> 163
+// and 185 -> 182 us).
+constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 57, 55, 59, 62, 61};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
@@ -487,6 +490,10 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
         case 58: return launch_half<N, 1, 3, true>(u, g, dx, w, E, stream);
         case 59: return launch_half<N, 2, 1, true>(u, g, dx, w, E, stream);
         case 60: return launch_half<N, 1, 4, true>(u, g, dx, w, E, stream);
+        // large n, the B stack aliasing U (dead after S1/S2: one stack less per
+        // element, one extra barrier): register ring + own element L2-prefetched
+        case 61: return try_pencil<N, 1, 2, false, 2, 2, 0, true, 0, true>(u, g, dx, w, E, stream);
+        case 62: return try_pencil<N, 1, 2, false, 3, 2, 0, true, 0, true>(u, g, dx, w, E, stream);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);

@@ -252,8 +252,17 @@ struct CgpArgs {
                           // metric copy is issued before griddep_wait)
 };
 
+// Doubles of layer stacks per slot: U, A, B -- or U and A only when B
+// aliases U (ALIAS: U is dead once S1/S2 have read it; one extra barrier).
+template <int N, bool ALIAS>
+constexpr int slot_doubles()
+{
+    using C = PencilCfg<N>;
+    return ALIAS ? (N * (C::LSU + C::LSA) + 1) / 2 * 2 : C::SLOT_DOUBLES;
+}
+
 template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0,
-          int GMODE = 0, bool FOLD = false, int CGM = 0>
+          int GMODE = 0, bool FOLD = false, int CGM = 0, bool ALIAS = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                  double* __restrict__ w, int64_t num_elements, const DParamP<N> D,
@@ -268,12 +277,15 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     const int p = tid - slot * NN;
     const bool lane_ok = slot < SLOTS;
     const int sl = lane_ok ? slot : 0;
-    double* U = smem + (size_t)sl * C::SLOT_DOUBLES;
+    static_assert(!ALIAS || (!PERSIST && CGM == 0 && GMODE < 2 && C::LSB == C::LSU),
+                  "B aliases U: one batch per CTA, U not needed after S2");
+    constexpr int SLOT_D = slot_doubles<N, ALIAS>();
+    double* U = smem + (size_t)sl * SLOT_D;
     double* A = U + N * LSU;
-    double* B = A + N * LSA;
+    double* B = ALIAS ? U : A + N * LSA;
     // GMODE >= 1: per-slot staged metric blocks after the slot stacks, then
     // the two mbarriers (u, g) shared by the CTA
-    double* Gbase = smem + ((size_t)SLOTS * C::SLOT_DOUBLES + 1) / 2 * 2;  // 16-B aligned
+    double* Gbase = smem + ((size_t)SLOTS * SLOT_D + 1) / 2 * 2;  // 16-B aligned
     double* G = Gbase + (size_t)sl * 6 * NNN;
     uint64_t* gbar = reinterpret_cast<uint64_t*>(Gbase + (GMODE ? (size_t)SLOTS * 6 * NNN : 0));
     uint64_t* ubar = gbar + 1;
@@ -423,7 +435,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                     mbar_expect_tx(ubar, (unsigned)(nact * NNN * 8));
                     for (int s2 = 0; s2 < nact; ++s2)
                         for (int k = 0; k < N; ++k)
-                            bulk_g2s(smem + (size_t)s2 * C::SLOT_DOUBLES + k * LSU,
+                            bulk_g2s(smem + (size_t)s2 * SLOT_D + k * LSU,
                                      u + (e0 + s2) * NNN + k * NN, NN * 8, ubar);
                 }
                 mbar_expect_tx(gbar, (unsigned)(nact * 6 * NNN * 8));
@@ -494,16 +506,21 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             stack_row_st<N>(A + ip_k * LSA + ip_j * RS, out);
         }
         // ---- S2: j-pencil (i,k): ws[j] = sum_l D[j][l] U[k][l][i] ----------
-        if (lane_ok) {
-            double col[N];
-            const double* src = U + jp_k * LSU + jp_i;
-#pragma unroll
-            for (int l = 0; l < N; ++l) col[l] = src[l * RS];
-            double* dst = B + jp_k * LSB + jp_i;
+        {
             double out[N];
-            pencil_gemv<N, FOLD, false>(D, kStS2, col, out);
+            if (lane_ok) {
+                double col[N];
+                const double* src = U + jp_k * LSU + jp_i;
 #pragma unroll
-            for (int j = 0; j < N; ++j) dst[j * RS] = out[j];
+                for (int l = 0; l < N; ++l) col[l] = src[l * RS];
+                pencil_gemv<N, FOLD, false>(D, kStS2, col, out);
+            }
+            if constexpr (ALIAS) __syncthreads();  // every U read done: B overwrites it
+            if (lane_ok) {
+                double* dst = B + jp_k * LSB + jp_i;
+#pragma unroll
+                for (int j = 0; j < N; ++j) dst[j * RS] = out[j];
+            }
         }
         __syncthreads();
 
