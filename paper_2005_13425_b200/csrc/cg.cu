@@ -264,7 +264,7 @@ static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_st
 // rank's partial -> state->local_sum, combined by sem_cg_finish).
 template <int N, bool DIST>
 __global__ void __launch_bounds__(kRowThreads, SEM_UPD_MINB)
-cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, Box bx,
+cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, BoxFlat bf,
                   sem_cg_state* st, double* history, ReduceScratch* rs,
                   const double* __restrict__ bot, const double* __restrict__ top,
                   bool deferred = false)
@@ -276,7 +276,8 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     double acc = 0.0;
     for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < E * NN;
          row += (int64_t)gridDim.x * kRowThreads) {
-        const Row<N> rw = make_row<N>(row, bx);
+        const Box& bx = bf.b;
+        const Row<N> rw = make_row<N>(row, bf);
         const int64_t base = rw.e * NNN + rw.jk * N;
         double v[N], rv[N];
         dssum_row<N>(w, rw, bx, DIST ? bot : nullptr, DIST ? top : nullptr, v);
@@ -305,8 +306,8 @@ static void launch_update(const double* w, double* r, int64_t E, const Box& bx, 
                           double* history, ReduceScratch* rs, const double* bot,
                           const double* top, cudaStream_t s)
 {
-    cg_update2_kernel<N, DIST><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, bx, st, history,
-                                                                     rs, bot, top);
+    cg_update2_kernel<N, DIST><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, make_box_flat(bx),
+                                                                     st, history, rs, bot, top);
 }
 
 // Finish a deferred reduction of the single-GPU iteration: the fixed-order
@@ -394,8 +395,8 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
         if (defer) {
             const unsigned ug = upd_grid<N>(E);
             if (int rc = chk(launch_k(cg_update2_kernel<N, false>, dim3(ug), dim3(kRowThreads), 0, s,
-                                      pdl, (const double*)w, r, E, bx, st, history, rs,
-                                      (const double*)nullptr, (const double*)nullptr, true),
+                                      pdl, (const double*)w, r, E, make_box_flat(bx), st, history,
+                                      rs, (const double*)nullptr, (const double*)nullptr, true),
                              "cg update kernel"))
                 return rc;
             if (int rc = chk(launch_k(cg_settle_kernel<2>, dim3(1), dim3(kSettleThreads), 0, s, pdl,
@@ -404,8 +405,8 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
                 return rc;
         } else {
             if (int rc = chk(launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
-                                      dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E, bx, st,
-                                      history, rs, (const double*)nullptr,
+                                      dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E,
+                                      make_box_flat(bx), st, history, rs, (const double*)nullptr,
                                       (const double*)nullptr, false),
                              "cg update kernel"))
                 return rc;

@@ -10,6 +10,7 @@
 // ascending-element order as gather_sum (box.cuh), hence bit-identical.
 #pragma once
 #include "box.cuh"
+#include "flat.cuh"
 
 namespace sem {
 
@@ -73,16 +74,26 @@ struct Row {
     bool x_hi_in;    // i = n-1 is not on the global x boundary (ix < ex-1)
 };
 
-template <int N>
-__device__ __forceinline__ Row<N> make_row(int64_t row, const Box& b)
+__device__ __forceinline__ const Box& box_of(const Box& b) { return b; }
+__device__ __forceinline__ const Box& box_of(const BoxFlat& bf) { return bf.b; }
+__device__ __forceinline__ ElemCoord elem_coord_of(int64_t e, const Box& b) { return elem_coord(e, b); }
+// magic-number division (no 64-bit divide on the row's critical path)
+__device__ __forceinline__ ElemCoord elem_coord_of(int64_t e, const BoxFlat& bf)
+{
+    return elem_coord_fast((uint32_t)e, bf);
+}
+
+template <int N, class BoxT>
+__device__ __forceinline__ Row<N> make_row(int64_t row, const BoxT& bt)
 {
     constexpr int NN = N * N;
+    const Box& b = box_of(bt);
     Row<N> r;
     r.e = row / NN;
     r.jk = (int)(row - r.e * NN);
     r.k = r.jk / N;
     r.j = r.jk - r.k * N;
-    r.c = elem_coord(r.e, b);
+    r.c = elem_coord_of(r.e, bt);
     const int gz = r.c.iz + b.gz0;
     r.yz_inner = axis_interior<N>(r.c.iy, r.j, b.ey) && axis_interior<N>(gz, r.k, b.ez_global);
     const int m = axis_mult<N>(r.c.iy, r.j, b.ey) * axis_mult<N>(gz, r.k, b.ez_global);
