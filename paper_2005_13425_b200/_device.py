@@ -6,6 +6,7 @@ unchanged."""
 from __future__ import annotations
 
 import ctypes
+import math
 import threading
 import weakref
 
@@ -131,7 +132,7 @@ class PinnedPool:
 
     def array(self, shape, dtype=np.float64) -> np.ndarray:
         """A fresh pinned numpy array; its memory is recycled after it dies."""
-        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        nbytes = math.prod(shape) * np.dtype(dtype).itemsize
         blk = self._take(max(nbytes, 1))
         arr = blk.numpy()[:nbytes].view(dtype).reshape(shape)
         weakref.finalize(arr, self._give, max(nbytes, 1), blk)

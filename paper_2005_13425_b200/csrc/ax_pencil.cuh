@@ -261,8 +261,20 @@ constexpr int slot_doubles()
     return ALIAS ? (N * (C::LSU + C::LSA) + 1) / 2 * 2 : C::SLOT_DOUBLES;
 }
 
+// bulk (TMA engine) store of a whole shared-memory block to global memory,
+// tracked as a bulk group; wait_read returns once the source has been read
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 template <int N, int SLOTS, int THREADS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0,
-          int GMODE = 0, bool FOLD = false, int CGM = 0, bool ALIAS = false>
+          int GMODE = 0, bool FOLD = false, int CGM = 0, bool ALIAS = false, bool WBULK = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                  double* __restrict__ w, int64_t num_elements, const DParamP<N> D,
@@ -593,7 +605,24 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         __syncthreads();
 
         // ---- S7: k-pencil: w = A + B + Wt ----------------------------------
-        if (active) {
+        if constexpr (WBULK) {
+            // WBULK: w staged contiguously in the (dead) metric block, then
+            // ONE bulk store of the element (large writes; for mapped host
+            // buffers, large PCIe write packets)
+            static_assert(GMODE == 1 && SLOTS == 1 && CGM == 0 && !PERSIST && N % 2 == 0,
+                          "WBULK: staged metric block reused, one element per CTA");
+            if (active) {
+#pragma unroll
+                for (int k = 0; k < N; ++k)
+                    G[k * NN + p] = (A[k * LSA + kp] + B[k * LSB + kp]) + Wt[k];
+            }
+            fence_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+                bulk_s2g(w + e * NNN, G, NNN * 8);
+                bulk_wait_read();
+            }
+        } else if (active) {
             double* we = w + e * NNN + p;
 #pragma unroll
             for (int k = 0; k < N; ++k) {

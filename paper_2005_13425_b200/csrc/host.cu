@@ -118,14 +118,20 @@ extern "C" int sem_ax_host(const double* u_host, const double* g, const double* 
     // Which side of the link each field crosses by copy engine and which by
     // the kernel's own loads/stores of mapped page-locked memory (UVA).
     // Pageable buffers have no device mapping and always use the copy engine.
-    int mode = kHostMode;
-    if (const char* env = getenv("SEM_HOST_MODE")) mode = atoi(env);  // tuning probe
+    static const int mode = getenv("SEM_HOST_MODE") ? atoi(getenv("SEM_HOST_MODE"))  // tuning probe
+                                                    : kHostMode;
     double* u_map = mapped(u_host);
     double* w_map = mapped(w_host);
     const bool zc_in = (mode == 1 || mode == 3) && u_map;
     const bool zc_out = (mode == 1 || mode == 2) && w_map;
-    if (zc_in && zc_out)  // one launch: PCIe reads and writes of all elements overlap
-        return ax_dispatch(u_map, g, dx, w_map, num_elements, n, 0, s);
+    if (zc_in && zc_out) {  // one launch: PCIe reads and writes of all elements overlap
+        // n = 10: each element's w leaves by ONE bulk (TMA) store -- larger
+        // PCIe write packets than per-thread stores (tools/wbulk_probe.py:
+        // 0.894 vs 0.904 ms; on device memory the bulk store is 5% slower,
+        // so device-resident calls keep the default)
+        const int zv = (n == 10) ? 63 : 0;
+        return ax_dispatch(u_map, g, dx, w_map, num_elements, n, zv, s);
+    }
     int64_t sizes[kMaxChunks];
     const int nchunks = chunk_schedule(num_elements, chunk_elements, sizes);
     cudaError_t err;
