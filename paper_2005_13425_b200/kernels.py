@@ -111,14 +111,32 @@ def _validate(u, g_shape, n: int) -> None:
         raise ValueError(f"geometry shape {tuple(g_shape)} does not match field {shp}")
 
 
+_basis_ptrs: dict = {}
+
+
+def _basis_host_ptrs(basis: PolynomialBasis):
+    """(dx, dxt) as contiguous float64 arrays with their ctypes pointers,
+    converted once per basis (the basis arrays are frozen)."""
+    ent = _basis_ptrs.get(id(basis))
+    if ent is None or ent[0] is not basis:
+        if len(_basis_ptrs) > 64:
+            _basis_ptrs.clear()
+        dx = np.ascontiguousarray(basis.diff, dtype=np.float64)
+        dxt = np.ascontiguousarray(basis.diff_t, dtype=np.float64)
+        ent = (basis, dx, dxt, dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt))
+        _basis_ptrs[id(basis)] = ent
+    return ent[3], ent[4]
+
+
 def apply_ax_into(u: torch.Tensor, g: torch.Tensor, basis: PolynomialBasis, w: torch.Tensor,
                   variant: int = 0) -> torch.Tensor:
-    """Device-only fast path: w <- A_local u (no validation, no allocation)."""
-    dx = np.ascontiguousarray(basis.diff, dtype=np.float64)
-    dxt = np.ascontiguousarray(basis.diff_t, dtype=np.float64)
-    check(load().sem_ax_variant(dv.ptr(u), dv.ptr(g), dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt),
-                                dv.ptr(w), int(u.shape[0]), int(basis.n), int(variant),
-                                dv.stream_handle(u.device)), "apply_ax")
+    """Device-only fast path: w <- A_local u (no validation, no allocation;
+    the per-call host work is a handful of attribute reads, so back-to-back
+    launches keep the GPU fed)."""
+    pdx, pdxt = _basis_host_ptrs(basis)
+    check(load().sem_ax_variant(u.data_ptr(), g.data_ptr(), pdx, pdxt, w.data_ptr(),
+                                u.shape[0], basis.n, variant,
+                                torch.cuda.current_stream(u.device).cuda_stream), "apply_ax")
     return w
 
 
@@ -224,23 +242,6 @@ def _host_device_scratch(dev: torch.device, numel: int):
         views = (ent[0][0, :numel], ent[0][1, :numel])
         ent[1][numel] = views
     return views
-
-
-_basis_ptrs: dict = {}
-
-
-def _basis_host_ptrs(basis: PolynomialBasis):
-    """(dx, dxt) as contiguous float64 arrays with their ctypes pointers,
-    converted once per basis (the basis arrays are frozen)."""
-    ent = _basis_ptrs.get(id(basis))
-    if ent is None or ent[0] is not basis:
-        if len(_basis_ptrs) > 64:
-            _basis_ptrs.clear()
-        dx = np.ascontiguousarray(basis.diff, dtype=np.float64)
-        dxt = np.ascontiguousarray(basis.diff_t, dtype=np.float64)
-        ent = (basis, dx, dxt, dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt))
-        _basis_ptrs[id(basis)] = ent
-    return ent[3], ent[4]
 
 
 def _apply_ax_host(u, kind: str, geom: GeomFactors, basis: PolynomialBasis):
