@@ -34,7 +34,10 @@ __all__ = ["CgConfig", "CgResult", "CgBreakdownError", "weighted_dot", "cg_solve
            "CG_VECTOR_FLOPS_PER_POINT", "CgWorkspace", "fused_phase_seconds"]
 
 CG_VECTOR_FLOPS_PER_POINT = 12
-USE_GRAPHS = True  # replay one captured iteration (fused path)
+USE_GRAPHS = True  # replay captured iterations (fused path)
+# iterations per captured graph: 1 measured best (tools/cg_graph_k.py: 5-20
+# iterations per graph ran 3-8% slower per iteration at E = 4096 and 32768)
+GRAPH_ITERATIONS = 1
 
 
 class CgBreakdownError(RuntimeError):
@@ -160,11 +163,18 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
             # iteration is captured into a CUDA graph and replayed: the
             # iteration's launches are parameter-stable (scalars live in the
             # device state), so replay == relaunch without the host overhead
+            # GRAPH_ITERATIONS iterations per graph: one graph launch per block
+            # of iterations instead of one per iteration; early exits are
+            # device-side (queued launches become no-ops)
             run(1)
-            key = (g.data_ptr(), box, dx.tobytes())
-            graph = ws.iteration_graph(lambda: run(1), key)
-            for _ in range(cfg.max_iterations - 1):
+            rest = cfg.max_iterations - 1
+            k = max(1, min(GRAPH_ITERATIONS, rest))
+            key = (g.data_ptr(), box, dx.tobytes(), k)
+            graph = ws.iteration_graph(lambda: run(k), key)
+            for _ in range(rest // k):
                 graph.replay()
+            if rest % k:
+                run(rest % k)
         else:
             run(cfg.max_iterations)
         finalize()
