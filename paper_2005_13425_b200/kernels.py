@@ -226,6 +226,10 @@ def _apply_ax_variant(u, kind: str, geom: GeomFactors, basis: PolynomialBasis,
 # elements per streamed chunk for host-buffer calls: 8 MB of u was the
 # best point of the chunk sweep on B200 + PCIe Gen5 (tools/e2e_probe.py)
 HOST_CHUNK_BYTES = 8 << 20
+# pieces a pageable input is staged in (host copy overlapping the GPU;
+# tools/numpy_e2e_probe.py: numpy in 1.50 ms unpiped, 1.15 / 1.19 / 1.32 ms with
+# 2 / 4 / 8 pieces, pinned input 0.92 ms)
+STAGE_CHUNKS = 2
 _host_scratch: dict = {}
 
 
@@ -262,19 +266,34 @@ def _apply_ax_host(u, kind: str, geom: GeomFactors, basis: PolynomialBasis):
     else:
         src = u if (u.dtype == torch.float64 and u.is_contiguous()) else \
             u.to(torch.float64).contiguous()
-    staged = None
-    if not src.is_pinned():  # stage pageable input through a recycled pinned block
-        staged = dv.pinned_pool.scratch(src.numel() * 8)
-        src = staged.view(torch.float64)[:src.numel()].view(shape).copy_(src)
     out_np = dv.pinned_pool.array(shape)
     pdx, pdxt = _basis_host_ptrs(basis)
     gd = geom.device_values(dev)
     ud, wd = _host_device_scratch(dev, E * n ** 3)
     stream = torch.cuda.current_stream()
     chunk = max(1, HOST_CHUNK_BYTES // (8 * n ** 3))
-    check(load().sem_ax_host(src.data_ptr(), gd.data_ptr(), pdx, pdxt,
-                             out_np.ctypes.data, E, n, ud.data_ptr(), wd.data_ptr(),
-                             chunk, stream.cuda_stream), "apply_ax")
+    lib = load()
+    per = n ** 3 * 8  # bytes per element of u / w
+    staged = None
+    if src.is_pinned():
+        check(lib.sem_ax_host(src.data_ptr(), gd.data_ptr(), pdx, pdxt,
+                              out_np.ctypes.data, E, n, ud.data_ptr(), wd.data_ptr(),
+                              chunk, stream.cuda_stream), "apply_ax")
+    else:
+        # pageable input (a reference-style numpy array): staged into a
+        # recycled pinned block in STAGE_CHUNKS pieces, each piece's apply
+        # enqueued as soon as it is staged, so the host copy of piece k+1
+        # overlaps the GPU's PCIe traffic for piece k
+        staged = dv.pinned_pool.scratch(src.numel() * 8)
+        st = staged.view(torch.float64)[:src.numel()].view(shape)
+        pieces = min(STAGE_CHUNKS, E)
+        for q in range(pieces):
+            e0, e1 = E * q // pieces, E * (q + 1) // pieces
+            st[e0:e1].copy_(src[e0:e1])
+            check(lib.sem_ax_host(st.data_ptr() + e0 * per, gd.data_ptr() + 6 * e0 * per,
+                                  pdx, pdxt, out_np.ctypes.data + e0 * per, e1 - e0, n,
+                                  ud.data_ptr() + e0 * per, wd.data_ptr() + e0 * per, chunk,
+                                  stream.cuda_stream), "apply_ax")
     stream.synchronize()
     if staged is not None:
         dv.pinned_pool.release(staged)
