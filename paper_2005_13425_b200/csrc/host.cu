@@ -118,8 +118,9 @@ extern "C" int sem_ax_host(const double* u_host, const double* g, const double* 
     // Which side of the link each field crosses by copy engine and which by
     // the kernel's own loads/stores of mapped page-locked memory (UVA).
     // Pageable buffers have no device mapping and always use the copy engine.
-    static const int mode = getenv("SEM_HOST_MODE") ? atoi(getenv("SEM_HOST_MODE"))  // tuning probe
-                                                    : kHostMode;
+    // read per call (tests switch it between calls): one environment lookup
+    int mode = kHostMode;
+    if (const char* env = getenv("SEM_HOST_MODE")) mode = atoi(env);
     double* u_map = mapped(u_host);
     double* w_map = mapped(w_host);
     const bool zc_in = (mode == 1 || mode == 3) && u_map;
