@@ -2,7 +2,7 @@
 
 The distributed driver (paper_2005_13425_b200/dist.py: partition, ordered
 two-step halo, rank-ordered scalar combine, CG choreography) runs here over
-world sizes 2 and 3 with a numpy implementation of the per-rank compute
+world sizes 2, 3 and 4 with a numpy implementation of the per-rank compute
 (test infrastructure; the product's per-rank compute is CudaSlabOps).  The
 distributed dssum must equal the GLOBAL oracle dssum bit-for-bit, and the
 distributed CG must reproduce the global oracle's residual history.
@@ -216,7 +216,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_dist_dssum_and_cg_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
