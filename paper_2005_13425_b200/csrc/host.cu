@@ -155,7 +155,8 @@ extern "C" int sem_ax_host(const double* u_host, const double* g, const double* 
             if (err == cudaSuccess) err = cudaStreamWaitEvent(s, ev_in, 0);
             if (err != cudaSuccess) return fail_cuda(err, "sem_ax_host: H2D");
         }
-        if (int rc = ax_dispatch(ku, g + e0 * 6 * per, dx, kw, e1 - e0, n, 0, s)) return rc;
+        const int cv = (zc_out && n == 10) ? 63 : 0;  // bulk-stored w into mapped memory
+        if (int rc = ax_dispatch(ku, g + e0 * 6 * per, dx, kw, e1 - e0, n, cv, s)) return rc;
         if (!zc_out) {
             err = cudaEventRecord(ev_k, s);
             if (err == cudaSuccess) err = cudaStreamWaitEvent(P->s_out, ev_k, 0);
