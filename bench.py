@@ -7,7 +7,11 @@ A "step" is one application of the local operator w = A_local u over all
 E=4096 elements of degree p=9 (n=10) with a random metric (BASELINE.json
 config 2, north_star).  Inputs are resident in HBM; the per-step working set
 (u + g + w = 262 MB) exceeds the 126 MB L2 and two input sets are rotated,
-so every step streams from HBM.  Prints ONE JSON line (rank 0).
+so every step streams from HBM.  Exactly K steps are timed (CUDA events,
+replays of a captured graph of --graph-steps applies + an eager remainder)
+right after the warm-up, with nvidia-smi clocks sampled inside the window;
+the `sustained` key repeats that after --soak seconds of load (power cap).
+Prints ONE JSON line (rank 0).
 
 Multi-GPU (torchrun, one rank per GPU): Ax is element-local, so each rank
 applies the operator to its own E=4096 elements (weak scaling, no
