@@ -228,11 +228,14 @@ static unsigned row_grid(int64_t E)
 }
 
 // update2 grid: ONE full wave of the row kernel -- SEM_UPD_MINB (6) blocks
-// per SM x 148 SMs -- each thread walking its rows grid-stride (tools/
-// upd_minb2.sh, profiles/r01_cg_tune.txt: 888 blocks at 80 registers beat
-// 740 at 86 and 1184 / 1776 / 2368, i.e. 1.3-2 waves, by 10-25%).  A
-// constant (a function of E and n only, never of the device), so the
-// reduction tree is fixed.
+// of 128 threads per SM x 148 SMs -- each thread walking its rows
+// grid-stride (tools/upd_minb2.sh: one wave beat 1.3-2 waves by 10-25%).
+// 3 x 256 threads measured ~1% faster per CG iteration (tools/
+// row_threads.sh, profiles/r01_cg_row_threads.txt) but its reduction tree
+// sent the reference's own manufactured-solution property (verify.py:
+// 457-476: 1331 iterations at tol 0, deep into FP64 underflow) into a
+// <p, A p> = 0 breakdown, so the verified tree is kept.  A constant (a
+// function of E and n only, never of the device), so the tree is fixed.
 constexpr int kUpdBlocks = SEM_UPD_MINB * 148;
 static_assert(kUpdBlocks <= kReduceBlocksMax, "update grid exceeds the partial slots");
 

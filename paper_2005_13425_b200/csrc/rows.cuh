@@ -14,7 +14,10 @@
 
 namespace sem {
 
-constexpr int kRowThreads = 128;
+#ifndef SEM_ROW_THREADS
+#define SEM_ROW_THREADS 128
+#endif
+constexpr int kRowThreads = SEM_ROW_THREADS;
 
 template <int N>
 __device__ __forceinline__ void load_row(const double* __restrict__ p, double (&v)[N])
