@@ -54,6 +54,14 @@ def max_over_ranks(value: float, dev) -> float:
     return float(t.item())
 
 
+def workload_config(world: int) -> dict:
+    """The `config` object both arms print (identical keys and strings)."""
+    return {"workload": f"Ax layered (sem_ax), E={E_HEAD} per GPU, p=9 (n=10), FP64, random gxyz",
+            "elements_per_gpu": E_HEAD, "n": N_HEAD,
+            "l2": "inputs larger than L2: 2 rotating sets of 262 MB",
+            "parallelism": f"dp{world} (element partition, no collective)"}
+
+
 def ax_flops(E, n):
     return E * n ** 3 * (12 * n + 15)  # sembench/kernels.py:121-125
 
@@ -166,6 +174,106 @@ def cpu_ax_sample(budget_s: float, reps_min: int = 3):
             "ms_per_apply": t * 1e3, "first_call_ms": t_one * 1e3}
 
 
+def _sembench():
+    """The UNMODIFIED reference package installed under baseline/_ref (pip
+    --target from /root/reference/pkg; it travels to the GPU box with the
+    snapshot).  Returns the module or raises ImportError."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "sembench")):
+        raise ImportError("baseline/_ref/sembench not installed")
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "sem_numba_cache"))
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import numba
+    import sembench
+    numba.set_num_threads(numba.config.NUMBA_NUM_THREADS)  # all host cores
+    return sembench
+
+
+def cpu_sembench_ax(budget_s: float, reps_min: int = 5):
+    """The reference itself (sembench.apply_ax, numba LAYERED kernel, all host
+    cores) on the full E=4096, p=9 apply: one JIT warm-up call, then the min
+    and median of >= reps_min reps."""
+    try:
+        S = _sembench()
+        import numba
+    except Exception as exc:  # noqa: BLE001 -- report, never fail the bench
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+    n, E = N_HEAD, E_HEAD
+    b = S.build_basis(n)
+    u = S.random_field(E, n, 1)
+    geom = S.GeomFactors(values=S.random_field(6 * E, n, 2).reshape(E, 6, n, n, n))
+    t0 = time.perf_counter()
+    S.apply_ax(u, geom, b, "layered")  # numba JIT / cache load
+    jit_s = time.perf_counter() - t0
+    times = []
+    start = time.perf_counter()
+    while len(times) < reps_min or (time.perf_counter() - start) < budget_s:
+        t0 = time.perf_counter()
+        S.apply_ax(u, geom, b, "layered")
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 500:
+            break
+    t = min(times)
+    return {"value": ax_flops(E, n) / t / 1e9, "unit": UNIT, "cores": numba.get_num_threads(),
+            "kind": "reference",
+            "sample": f"sembench.apply_ax(variant='layered') full E={E}, p=9, {len(times)} reps "
+                      f"(min; median {statistics.median(times) * 1e3:.2f} ms), numba "
+                      f"{numba.__version__}, cpu={_cpu_model()}",
+            "ms_per_apply": t * 1e3, "ms_per_apply_median": statistics.median(times) * 1e3,
+            "first_call_s": jit_s}
+
+
+def cpu_cg_sample(iters: int = 5):
+    """CPU CG beside cg_e4096_p9 (BASELINE config 4): the reference's
+    cg_solve(apply_global) on the bench recipe (sembench/bench.py:140-166)
+    for `iters` iterations, and the oracle port's CG on the same RHS.
+    Milliseconds per iteration; the 100-iteration run scales linearly."""
+    out = {}
+    n, E = N_HEAD, E_HEAD
+    try:
+        S = _sembench()
+        import numba
+        ex, ey, ez = S.factor_elements(E)
+        b = S.build_basis(n)
+        mesh = S.build_mesh(ex, ey, ez, n, 1.0)
+        topo, geom = S.build_topology(mesh), S.build_geom(mesh, b)
+        from sembench.fields import mix64
+        f = S.make_rhs(E, n, topo, mix64(1, E))
+        op = lambda p: S.apply_global(p, geom, b, topo)  # noqa: E731
+        S.cg_solve(f, op, topo, S.CgConfig(1, 0.0))  # JIT warm-up
+        t0 = time.perf_counter()
+        res = S.cg_solve(f, op, topo, S.CgConfig(iters, 0.0))
+        dt = (time.perf_counter() - t0) / iters
+        out["sembench"] = {"ms_per_iteration": dt * 1e3, "iterations": iters,
+                           "cores": numba.get_num_threads(), "kind": "reference",
+                           "final_residual": float(res.residual_history[-1]),
+                           "what": "sembench.cg_solve(apply_global) numba + numpy, "
+                                   f"E={E}, p=9, cpu={_cpu_model()}"}
+    except Exception as exc:  # noqa: BLE001
+        out["sembench"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
+    try:
+        import oracle as O
+        from paper_2005_13425_b200.basis import build_basis
+        b = build_basis(n)
+        ex, ey, ez = O.factor_elements(E)
+        T = O.BoxTopology(ex, ey, ez, n)
+        gh = O.box_geom(ex, ey, ez, b.weights, 1.0)
+        f = O.mask(O.dssum(O.random_field(E, n, O.mix64(1, E)), T), T)
+        th = O.max_threads()
+        op = lambda p: O.apply_global(p, gh, b.diff, b.diff_t, T, th)  # noqa: E731
+        O.cg(f, op, T, 1, nthreads=th)
+        t0 = time.perf_counter()
+        _, hist, _ = O.cg(f, op, T, iters, nthreads=th)
+        dt = (time.perf_counter() - t0) / iters
+        out["port"] = {"ms_per_iteration": dt * 1e3, "iterations": iters, "cores": th,
+                       "kind": "port", "final_residual": float(hist[-1]),
+                       "what": "oracle/sem_oracle.c Ax + ordered dssum (C, OpenMP) + numpy CG"}
+    except Exception as exc:  # noqa: BLE001
+        out["port"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
+    return out
+
+
 def _cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as fh:
@@ -179,50 +287,62 @@ def _cpu_model() -> str:
 
 # ------------------------------------------------------------ reference ----
 def run_reference(args, rank, world):
+    """The reference arm: the reference's own CPU implementation of the path
+    on the host cores, same config / metric as our arm.  `value` is the
+    UNMODIFIED reference package (sembench from baseline/_ref, its public
+    `apply_ax(..., "layered")`, numba over all host cores) on the full
+    E=4096, p=9 apply; the oracle's C port is timed beside it
+    (cpu_baseline.port).  Without baseline/_ref the port is the value."""
     if rank != 0:
         return 0
-    import oracle as O
-    from paper_2005_13425_b200.basis import build_basis
-    b = build_basis(N_HEAD)
-    E = E_HEAD
-    u = O.random_field(E, N_HEAD, 1)
-    g = O.random_field(6 * E, N_HEAD, 2).reshape(E, 6, N_HEAD, N_HEAD, N_HEAD)
-    threads = O.max_threads()
-    t0 = time.perf_counter()
-    O.ax_layered(u, g, b.diff, b.diff_t, threads)
-    t_full = time.perf_counter() - t0
-    # bound the whole run to ~90 s: shrink the per-step element sample if needed
-    budget = 90.0
-    frac = min(1.0, budget / max(1e-9, (args.steps + args.warmup) * t_full))
-    Es = max(1, int(E * frac))
-    us, gs = np.ascontiguousarray(u[:Es]), np.ascontiguousarray(g[:Es])
-    # warm-up: the W steps, and at least ~1 s so the thread pool and the
+    n, E = N_HEAD, E_HEAD
+    try:
+        S = _sembench()
+        import numba
+        b = S.build_basis(n)
+        u = S.random_field(E, n, 1)
+        geom = S.GeomFactors(values=S.random_field(6 * E, n, 2).reshape(E, 6, n, n, n))
+        call = lambda: S.apply_ax(u, geom, b, "layered")  # noqa: E731
+        cores, kind = numba.get_num_threads(), "reference"
+        what = (f"sembench.apply_ax(variant='layered') from baseline/_ref (unmodified "
+                f"reference, numba {numba.__version__}), full E={E} apply per step")
+    except Exception as exc:  # noqa: BLE001
+        import oracle as O
+        from paper_2005_13425_b200.basis import build_basis
+        b = build_basis(n)
+        u = O.random_field(E, n, 1)
+        g = O.random_field(6 * E, n, 2).reshape(E, 6, n, n, n)
+        cores, kind = O.max_threads(), "port"
+        call = lambda: O.ax_layered(u, g, b.diff, b.diff_t, cores)  # noqa: E731
+        what = (f"oracle/sem_oracle.c (restatement of sembench/kernels.py:267-329), full "
+                f"E={E} apply per step; sembench unavailable: {type(exc).__name__}: {exc}")
+    # warm-up: JIT, the W steps, and at least ~1 s so the thread pool and the
     # cores' clocks have settled (the first calls of a fresh process run up
     # to 1.5x slower)
     t_w = time.perf_counter()
     done = 0
-    while done < args.warmup or time.perf_counter() - t_w < 1.0:
-        O.ax_layered(us, gs, b.diff, b.diff_t, threads)
+    while done < args.warmup + 1 or time.perf_counter() - t_w < 1.0:
+        call()
         done += 1
     per = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
         t1 = time.perf_counter()
-        O.ax_layered(us, gs, b.diff, b.diff_t, threads)
+        call()
         per.append(time.perf_counter() - t1)
     dt = (time.perf_counter() - t0) / args.steps
-    val = ax_flops(Es, N_HEAD) / dt / 1e9
+    val = ax_flops(E, n) / dt / 1e9
+    port = None
+    if kind == "reference" and not args.no_cpu:
+        port = cpu_ax_sample(args.cpu_budget / 2)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded SplitMix64 u and random metric g, sembench/fields.py)",
-        "config": {"workload": f"Ax layered, E={E}, p=9 (n=10), FP64, random gxyz",
-                   "elements_per_step": Es},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{Es} of {E} elements per step, oracle/sem_oracle.c "
-                                   f"(restatement of sembench/kernels.py:267-329), "
-                                   f"cpu={_cpu_model()}"},
+        "data": "synthetic (seeded SplitMix64 u and random metric g, generated on device)",
+        "config": workload_config(world),
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{what}, cpu={_cpu_model()}", "port": port},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
         "step_ms": {"median": statistics.median(per) * 1e3, "min": min(per) * 1e3,
@@ -293,9 +413,18 @@ def run_ours(args, rank, world, local_rank):
             else:
                 dist.barrier()
 
+    # warm-up: the W steps eagerly, then the captured graph replayed (its
+    # first launch uploads it; nothing first-time may land in the window)
     for i in range(max(args.warmup, 3)):
         step(i)
+    if graph is not None:
+        for _ in range(3):
+            graph.replay()
     torch.cuda.synchronize(dev)
+    # a warm burst of >= --warm-ms of graph-replayed applies runs right before
+    # every timed window (after the clock sampler is delivering), so the
+    # window opens on a GPU that is already streaming at its clocks
+    warm_steps = max(1, int(args.warm_ms * 1e-3 / 41e-6))
 
     def timed_region(soak: float):
         """(ms per step over exactly args.steps steps, clock summary of the
@@ -307,7 +436,9 @@ def run_ours(args, rank, world, local_rank):
                 run_steps(200)
                 torch.cuda.synchronize(dev)
             barrier()
-            torch.cuda.synchronize(dev)
+            run_steps(warm_steps)
+            if args.warm_sync:
+                torch.cuda.synchronize(dev)
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0 = time.perf_counter()
             ev0.record(stream)
@@ -407,7 +538,16 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_ax_sample(args.cpu_budget)
+        # the reference itself (sembench, numba, all cores) when installed,
+        # the oracle's C port beside it
+        port = cpu_ax_sample(args.cpu_budget / 2)
+        ref = cpu_sembench_ax(args.cpu_budget / 2)
+        if "unavailable" in ref:
+            cpu = dict(port, sembench=ref)
+        else:
+            cpu = dict(ref, port=port)
+        if cg is not None:
+            cg["cpu"] = cpu_cg_sample(args.cpu_cg_iters)
 
     if rank == 0:
         line = {
@@ -415,10 +555,7 @@ def run_ours(args, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded SplitMix64 u and random metric g, generated on device)",
-            "config": {"workload": f"Ax layered (sem_ax), E={E} per GPU, p=9 (n=10), FP64, "
-                                   "random gxyz", "elements_per_gpu": E, "n": n,
-                       "l2": "inputs larger than L2: 2 rotating sets of 262 MB",
-                       "parallelism": f"dp{world} (element partition, no collective)"},
+            "config": workload_config(world),
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": achieved_gbs / hbm, "traffic": traffic,
                          "peak_source": peaks.get("source"),
@@ -629,9 +766,15 @@ def main(argv=None):
                     help="seconds of load before the `sustained` timed region")
     ap.add_argument("--graph-steps", type=int, default=50,
                     help="applies per captured CUDA graph in the timed loop (0: eager launches)")
+    ap.add_argument("--warm-ms", type=float, default=40.0,
+                    help="milliseconds of graph-replayed applies right before each timed window")
+    ap.add_argument("--warm-sync", type=int, default=1,
+                    help="synchronize between the warm burst and the timed window")
     ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-cg-iters", type=int, default=5,
+                    help="CG iterations timed on the CPU beside cg_e4096_p9")
     ap.add_argument("--cg", type=int, default=1)
     ap.add_argument("--ax-sizes", type=int, default=1, help="also time E=1024/2048 (config 2)")
     ap.add_argument("--cg-weak", type=int, default=1)
