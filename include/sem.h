@@ -107,6 +107,23 @@ int sem_dssum_box(const double *f, double *out, int32_t ex, int32_t ey, int32_t 
                   int32_t n, int32_t apply_mask, sem_stream_t stream);
 int sem_mask_box(const double *f, double *out, int32_t ex, int32_t ey, int32_t ez,
                  int32_t n, sem_stream_t stream);
+/* General numbering (any reference Topology.global_id, assembly.py:113-120):
+ * the id classes as a CSR -- seg_idx = local flat indices grouped by global
+ * id, each group in ascending local index (a stable argsort of global_id);
+ * seg_off[nseg+1] delimits the groups.  Each class is summed in that order
+ * from +0.0 (np.bincount's order) and the total written to every copy:
+ * bit-identical to the reference for any numbering.  Out-of-place. */
+int sem_dssum_csr(const double *f, double *out, const int32_t *seg_off,
+                  const int32_t *seg_idx, int64_t nseg, sem_stream_t stream);
+/* out = f * mask pointwise (assembly.py:123-129 with an arbitrary mask array). */
+int sem_mask_array(const double *f, const double *mask, double *out, int64_t count,
+                   sem_stream_t stream);
+/* flag_dev[0] <- 0 if every unmasked shared node of f has equal copies
+ * (f is interface-consistent on the box), else 1.  The fused CG's local
+ * <p, A p> equals the reference's assembled one (cg.py:163) only for
+ * consistent iterates; cg_solve checks mask(f) with this first. */
+int sem_consistent_box(const double *f, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+                       int32_t *flag_dev, sem_stream_t stream);
 /* mask(dssum(A_local(mask(u)))) with `scratch` an E*n^3 float64 buffer. */
 int sem_apply_global(const double *u, const double *g, const double *dx,
                      const double *dxt, double *w, double *scratch, int32_t ex,

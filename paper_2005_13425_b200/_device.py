@@ -8,6 +8,7 @@ from __future__ import annotations
 import ctypes
 import math
 import threading
+import warnings
 import weakref
 
 import numpy as np
@@ -49,7 +50,10 @@ def as_device_f64(x, device: torch.device | None = None, name: str = "array") ->
     if isinstance(x, np.ndarray):
         dev = device or current_device()
         arr = np.ascontiguousarray(x, dtype=np.float64)
-        return torch.from_numpy(arr).to(dev, non_blocking=False)
+        with warnings.catch_warnings():  # read-only arrays (frozen geometry) are only read
+            warnings.simplefilter("ignore", UserWarning)
+            src = torch.from_numpy(arr)
+        return src.to(dev, non_blocking=False)
     raise ValueError(f"{name} must be a numpy array or a torch tensor, got {type(x).__name__}")
 
 
@@ -133,9 +137,16 @@ class PinnedPool:
     def array(self, shape, dtype=np.float64) -> np.ndarray:
         """A fresh pinned numpy array; its memory is recycled after it dies."""
         nbytes = math.prod(shape) * np.dtype(dtype).itemsize
-        blk = self._take(max(nbytes, 1))
-        arr = blk.numpy()[:nbytes].view(dtype).reshape(shape)
-        weakref.finalize(arr, self._give, max(nbytes, 1), blk)
+        size = max(nbytes, 1)
+        blk = self._take(size)
+        # a per-call owner object exports the block's memory; every numpy
+        # view (and torch.from_numpy of one) chains its .base to it, so the
+        # block is recycled only when the LAST view dies -- a finalizer on the
+        # returned array itself would fire while a reshape/ravel view lives
+        owner = (ctypes.c_char * size).from_address(blk.data_ptr())
+        owner._block = blk
+        weakref.finalize(owner, self._give, size, blk)
+        arr = np.frombuffer(owner, dtype=np.uint8, count=nbytes).view(dtype).reshape(shape)
         return arr
 
     def scratch(self, nbytes: int) -> torch.Tensor:

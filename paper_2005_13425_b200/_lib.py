@@ -60,6 +60,9 @@ SIGNATURES = {
     "sem_ax_host": (ctypes.c_int, [_vp, _vp, _dp, _dp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
     "sem_dssum_box": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
     "sem_mask_box": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    "sem_dssum_csr": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
+    "sem_mask_array": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp]),
+    "sem_consistent_box": (ctypes.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "sem_apply_global": (ctypes.c_int, [_vp, _vp, _dp, _dp, _vp, _vp, _i32, _i32, _i32, _i32,
                                         _vp]),
     "sem_add2s1": (ctypes.c_int, [_vp, _vp, _f64, _i64, _vp]),

@@ -11,7 +11,7 @@ reference's integer recipe, for callers that inspect them.
 
 from __future__ import annotations
 
-import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -22,10 +22,10 @@ from ._lib import check, load
 from .basis import PolynomialBasis
 from .fields import validate_field
 from .kernels import KernelVariant, TrafficCounters, apply_ax
-from .mesh import BoxMesh, GeomFactors
+from .mesh import BoxMesh, GeomFactors, as_geom
 
-__all__ = ["Topology", "OperatorTimers", "build_topology", "dssum", "mask", "apply_global",
-           "GlobalOperator"]
+__all__ = ["Topology", "CsrTopology", "OperatorTimers", "build_topology", "as_topology",
+           "dssum", "mask", "apply_global", "GlobalOperator"]
 
 
 @dataclass(frozen=True)
@@ -110,17 +110,163 @@ def build_topology(mesh: BoxMesh) -> Topology:
                     num_global=num_global)
 
 
-def _dssum_dev(f: torch.Tensor, topo: Topology, apply_mask: bool) -> torch.Tensor:
+class CsrTopology:
+    """A reference-style topology whose numbering is NOT the box lattice.
+
+    Built from any object carrying the reference ``Topology`` fields
+    (``num_elements``, ``n``, ``num_global``, ``global_id``, ``mask``,
+    ``multiplicity``, ``inv_multiplicity``; sembench/assembly.py:37-53).
+    dssum runs the ordered CSR gather (``sem_dssum_csr``: each id class
+    summed in ascending local index from +0.0, bit-identical to the
+    reference's ``np.bincount``), mask multiplies by the caller's mask array
+    (``sem_mask_array``), weighted dots read ``inv_multiplicity``
+    (``sem_glsc3``).  The device copies are made once per device.
+    """
+
+    def __init__(self, src):
+        self.num_elements = int(src.num_elements)
+        self.n = int(src.n)
+        self.num_global = int(src.num_global)
+        shape = (self.num_elements, self.n, self.n, self.n)
+        self.global_id = np.asarray(src.global_id).reshape(shape)
+        self.multiplicity = np.asarray(src.multiplicity).reshape(shape)
+        self.mask = np.asarray(src.mask, dtype=np.float64).reshape(shape)
+        self.inv_multiplicity = np.asarray(src.inv_multiplicity, dtype=np.float64).ravel()
+        gid = self.global_id.ravel().astype(np.int64, copy=False)
+        if gid.size >= 2 ** 31:
+            raise ValueError("general topologies are limited to 2^31 - 1 local points")
+        if gid.size and (gid.min() < 0 or gid.max() >= self.num_global):
+            raise ValueError("global_id outside [0, num_global)")
+        counts = np.bincount(gid, minlength=self.num_global)
+        self._off = np.zeros(self.num_global + 1, dtype=np.int32)
+        np.cumsum(counts, out=self._off[1:])
+        self._idx = np.argsort(gid, kind="stable").astype(np.int32)
+        self._dev: dict = {}
+
+    @property
+    def dofs(self) -> int:
+        return self.num_elements * self.n ** 3
+
+    def device_arrays(self, device: torch.device):
+        """(seg_off, seg_idx, mask, inv_multiplicity) on `device`."""
+        ent = self._dev.get(device.index)
+        if ent is None:
+            ent = tuple(torch.from_numpy(np.array(a)).to(device) for a in
+                        (self._off, self._idx, self.mask, self.inv_multiplicity))
+            self._dev[device.index] = ent
+        return ent
+
+
+_converted: dict = {}
+
+
+def _box_of(t):
+    """The (ex, ey, ez) box whose lattice numbering t.global_id might be, or None."""
+    n, E = int(t.n), int(t.num_elements)
+    gid = np.asarray(t.global_id)
+    if E < 1 or n < 2 or gid.shape != (E, n, n, n) or int(gid[0, 0, 0, 0]) != 0:
+        return None
+    nx = int(gid[0, 0, 1, 0])
+    if nx < n or (nx - 1) % (n - 1):
+        return None
+    ny = int(gid[0, 1, 0, 0]) // nx
+    if ny < n or (ny - 1) % (n - 1):
+        return None
+    ex, ey = (nx - 1) // (n - 1), (ny - 1) // (n - 1)
+    if E % (ex * ey):
+        return None
+    return ex, ey, E // (ex * ey)
+
+
+def as_topology(topo):
+    """This package's topology for `topo`.
+
+    Our own :class:`Topology` / :class:`CsrTopology` pass through.  Any other
+    object with the reference ``Topology`` fields (e.g. one built by
+    ``sembench.build_topology``) is checked against the box lattice: when
+    its ``global_id``, ``multiplicity``, ``mask`` and ``inv_multiplicity``
+    are exactly the lattice's (assembly.py:69-110), the analytic box
+    topology is returned (every fused kernel applies); otherwise a
+    :class:`CsrTopology` (general ordered gather).  Conversions of objects
+    whose arrays are read-only are cached."""
+    if isinstance(topo, (Topology, CsrTopology)):
+        return topo
+    needed = ("num_elements", "n", "num_global", "global_id", "multiplicity", "mask",
+              "inv_multiplicity")
+    if not all(hasattr(topo, a) for a in needed):
+        raise TypeError(f"not a topology: {type(topo).__name__} lacks the reference "
+                        "Topology fields")
+    ent = _converted.get(id(topo))
+    if ent is not None and ent[0]() is topo:
+        return ent[1]
+    frozen = all(not getattr(getattr(topo, a), "flags", None) or
+                 not getattr(topo, a).flags.writeable
+                 for a in ("global_id", "multiplicity", "mask", "inv_multiplicity"))
+    box = _box_of(topo)
+    out = None
+    if box is not None:
+        cand = build_topology(BoxMesh(*box, int(topo.n), 1.0))
+        if cand.num_global == int(topo.num_global) and \
+                np.array_equal(cand.global_id, np.asarray(topo.global_id)) and \
+                np.array_equal(cand.multiplicity, np.asarray(topo.multiplicity)) and \
+                np.array_equal(cand.mask, np.asarray(topo.mask)) and \
+                np.array_equal(cand.inv_multiplicity, np.asarray(topo.inv_multiplicity).ravel()):
+            out = cand
+    if out is None:
+        out = CsrTopology(topo)
+    if frozen:
+        try:
+            ref = weakref.ref(topo)
+        except TypeError:
+            return out
+        if len(_converted) > 64:
+            _converted.clear()
+        _converted[id(topo)] = (ref, out)
+    return out
+
+
+def _dssum_dev(f: torch.Tensor, topo, apply_mask: bool) -> torch.Tensor:
     out = torch.empty_like(f)
+    if isinstance(topo, CsrTopology):
+        off, idx, msk, _ = topo.device_arrays(f.device)
+        s = dv.stream_handle(f.device)
+        check(load().sem_dssum_csr(dv.ptr(f), dv.ptr(out), dv.ptr(off), dv.ptr(idx),
+                                   topo.num_global, s), "dssum")
+        if apply_mask:
+            check(load().sem_mask_array(dv.ptr(out), dv.ptr(msk), dv.ptr(out), out.numel(), s),
+                  "mask")
+        return out
     check(load().sem_dssum_box(dv.ptr(f), dv.ptr(out), topo.ex, topo.ey, topo.ez, topo.n,
                                1 if apply_mask else 0, dv.stream_handle(f.device)), "dssum")
     return out
 
 
-def _mask_dev(f: torch.Tensor, topo: Topology) -> torch.Tensor:
+def _mask_dev(f: torch.Tensor, topo) -> torch.Tensor:
     out = torch.empty_like(f)
+    if isinstance(topo, CsrTopology):
+        msk = topo.device_arrays(f.device)[2]
+        check(load().sem_mask_array(dv.ptr(f), dv.ptr(msk), dv.ptr(out), out.numel(),
+                                    dv.stream_handle(f.device)), "mask")
+        return out
     check(load().sem_mask_box(dv.ptr(f), dv.ptr(out), topo.ex, topo.ey, topo.ez, topo.n,
                               dv.stream_handle(f.device)), "mask")
+    return out
+
+
+def _wdot_dev(a: torch.Tensor, b: torch.Tensor, topo, out: torch.Tensor | None = None
+              ) -> torch.Tensor:
+    """<a, b>_c = sum(a * b * inv_multiplicity) into a device scalar."""
+    dev = a.device
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=dev)
+    s, scratch = dv.stream_handle(dev), dv.reduce_scratch(dev)
+    if isinstance(topo, CsrTopology):
+        invm = topo.device_arrays(dev)[3]
+        check(load().sem_glsc3(dv.ptr(a), dv.ptr(b), dv.ptr(invm), a.numel(), dv.ptr(out),
+                               dv.ptr(scratch), s), "weighted_dot")
+    else:
+        check(load().sem_glsc3_box(dv.ptr(a), dv.ptr(b), topo.ex, topo.ey, topo.ez, topo.n,
+                                   dv.ptr(out), dv.ptr(scratch), s), "weighted_dot")
     return out
 
 
@@ -128,6 +274,7 @@ def dssum(f, topo: Topology, counters: TrafficCounters | None = None):
     """Sum every class of coincident nodes; all copies receive the total.
 
     Bit-identical to the reference's ``np.bincount`` order."""
+    topo = as_topology(topo)
     validate_field(f, topo.num_elements, topo.n)
     fd, kind = dv.to_device_io(f, "f")
     with torch.cuda.device(fd.device):
@@ -139,6 +286,7 @@ def dssum(f, topo: Topology, counters: TrafficCounters | None = None):
 
 def mask(f, topo: Topology, counters: TrafficCounters | None = None):
     """Zero the boundary nodes (pointwise product with the 0/1 mask)."""
+    topo = as_topology(topo)
     validate_field(f, topo.num_elements, topo.n)
     fd, kind = dv.to_device_io(f, "f")
     with torch.cuda.device(fd.device):
@@ -153,10 +301,14 @@ def apply_global(u, geom: GeomFactors, basis: PolynomialBasis, topo: Topology,
                  counters: TrafficCounters | None = None,
                  timers: OperatorTimers | None = None, workspace=None):
     """Global masked Poisson operator mask(dssum(A_local(mask(u))))."""
+    topo = as_topology(topo)
+    geom = as_geom(geom)
     validate_field(u, topo.num_elements, topo.n)
     ud, kind = dv.to_device_io(u, "u")
     with torch.cuda.device(ud.device):
-        um = mask(ud, topo, counters)
+        um = _mask_dev(ud, topo)
+        if counters is not None:
+            counters.add(reads=2 * topo.dofs, writes=topo.dofs)
         if timers is None:
             w = apply_ax(um, geom, basis, variant, counters, workspace)
             w = _dssum_dev(w, topo, True)
@@ -187,6 +339,7 @@ class GlobalOperator:
 
     def __init__(self, geom: GeomFactors, basis: PolynomialBasis, topo: Topology,
                  counters: TrafficCounters | None = None, timers: OperatorTimers | None = None):
+        geom, topo = as_geom(geom), as_topology(topo)
         if basis.n != topo.n or geom.n != topo.n or geom.num_elements != topo.num_elements:
             raise ValueError("geometry, basis and topology disagree on n or element count")
         self.geom, self.basis, self.topo = geom, basis, topo

@@ -26,7 +26,7 @@ import torch
 
 from . import _device as dv
 from ._lib import check, load, sem_cg_state
-from .assembly import GlobalOperator, Topology, _mask_dev
+from .assembly import GlobalOperator, Topology, _mask_dev, _wdot_dev, as_topology
 from .fields import validate_field
 from .kernels import TrafficCounters
 
@@ -38,6 +38,9 @@ USE_GRAPHS = True  # replay captured iterations (fused path)
 # iterations per captured graph: 1 measured best (tools/cg_graph_k.py: 5-20
 # iterations per graph ran 3-8% slower per iteration at E = 4096 and 32768)
 GRAPH_ITERATIONS = 1
+# graph replays between non-blocking polls of the device stop flag
+POLL_EVERY = 8
+_STOP_OFFSET = sem_cg_state.stop.offset
 
 
 class CgBreakdownError(RuntimeError):
@@ -64,19 +67,14 @@ class CgResult:
     counters: TrafficCounters = field(default_factory=TrafficCounters)
 
 
-def _glsc3_box_dev(a: torch.Tensor, b: torch.Tensor, topo: Topology,
+def _glsc3_box_dev(a: torch.Tensor, b: torch.Tensor, topo,
                    out: torch.Tensor | None = None) -> torch.Tensor:
-    dev = a.device
-    if out is None:
-        out = torch.empty(1, dtype=torch.float64, device=dev)
-    check(load().sem_glsc3_box(dv.ptr(a), dv.ptr(b), topo.ex, topo.ey, topo.ez, topo.n,
-                               dv.ptr(out), dv.ptr(dv.reduce_scratch(dev)),
-                               dv.stream_handle(dev)), "weighted_dot")
-    return out
+    return _wdot_dev(a, b, topo, out)
 
 
-def weighted_dot(u, v, topo: Topology) -> float:
+def weighted_dot(u, v, topo) -> float:
     """sum(u * v / multiplicity) -- deterministic device reduction."""
+    topo = as_topology(topo)
     validate_field(u, topo.num_elements, topo.n, "u")
     validate_field(v, topo.num_elements, topo.n, "v")
     dev = u.device if dv.is_tensor(u) else (v.device if dv.is_tensor(v) else None)
@@ -87,11 +85,22 @@ def weighted_dot(u, v, topo: Topology) -> float:
         return float(out.item())
 
 
+def _consistent(f_dev: torch.Tensor, topo: Topology) -> bool:
+    """Is mask(f) interface-consistent (equal copies of every shared node)?"""
+    flag = torch.empty(1, dtype=torch.int32, device=f_dev.device)
+    check(load().sem_consistent_box(dv.ptr(f_dev), topo.ex, topo.ey, topo.ez, topo.n,
+                                    dv.ptr(flag), dv.stream_handle(f_dev.device)),
+          "cg_solve consistency check")
+    return int(flag.item()) == 0
+
+
 class CgWorkspace:
     """Device vectors and state of one fused solve (reusable across solves)."""
 
     def __init__(self, topo: Topology, max_iterations: int, device: torch.device):
+        topo = as_topology(topo)
         shape = (topo.num_elements, topo.n, topo.n, topo.n)
+        self.box = (topo.ex, topo.ey, topo.ez, topo.n)
         mk = lambda: torch.empty(shape, dtype=torch.float64, device=device)  # noqa: E731
         self.x, self.r, self.p = mk(), mk(), mk()
         self.w = torch.empty((2,) + shape, dtype=torch.float64, device=device)
@@ -103,6 +112,15 @@ class CgWorkspace:
         self.max_iterations = max_iterations
         self._graph = None
         self._graph_key = None
+        # pinned mirror of state.stop for the replay loop's non-blocking poll
+        self._stop_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self._stop_event = None
+
+    def fits(self, topo: Topology, max_iterations: int, device: torch.device) -> bool:
+        """Usable for a solve on `topo` (same box and n: the launches index the
+        vectors by the box) with this iteration budget on this device."""
+        return (self.box == (topo.ex, topo.ey, topo.ez, topo.n)
+                and self.max_iterations >= max_iterations and self.device == device)
 
     def iteration_graph(self, launch_one, key):
         """CUDA graph of one fused iteration (captured once per workspace and
@@ -133,7 +151,7 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
                  callback, host: bool, ws: CgWorkspace | None = None):
     lib = load()
     dev = f_dev.device
-    if ws is None or ws.max_iterations < cfg.max_iterations or ws.device != dev:
+    if ws is None or not ws.fits(topo, cfg.max_iterations, dev):
         ws = CgWorkspace(topo, cfg.max_iterations, dev)
     s = dv.stream_handle(dev)
     g = op.geom.device_values(dev)
@@ -157,24 +175,53 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
         check(lib.sem_cg_finalize(dv.ptr(ws.x), dv.ptr(ws.p), dv.ptr(ws.state), m,
                                   dv.stream_handle(dev)), "cg_solve finalize")
 
-    if callback is None:
+    timers = op.timers
+    if callback is None and timers is not None:
+        # the same launches with CUDA events between them (sem_cg_run_phases):
+        # the operator's timers receive the device time of the Ax phase (Ax
+        # with the fused p update and <p, A p>) and of the assembly phase
+        # (dssum + mask fused with the r update and <r, r>)
+        import ctypes
+        ms = (ctypes.c_double * 3)(0.0, 0.0, 0.0)
+        check(lib.sem_cg_run_phases(dv.ptr(g), dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt),
+                                    dv.ptr(ws.x), dv.ptr(ws.r), dv.ptr(ws.p), dv.ptr(ws.w),
+                                    dv.ptr(ws.state), dv.ptr(ws.history), cfg.max_iterations,
+                                    *box, dv.ptr(ws.scratch), ms, s), "cg_solve run")
+        timers.ax_seconds += ms[0] * 1e-3
+        timers.dssum_seconds += (ms[1] + ms[2]) * 1e-3
+        finalize()
+        st = ws.read_state()
+    elif callback is None:
         if cfg.max_iterations > 2 and USE_GRAPHS:
             # iteration 1 launched directly (configures the kernels), then one
             # iteration is captured into a CUDA graph and replayed: the
             # iteration's launches are parameter-stable (scalars live in the
-            # device state), so replay == relaunch without the host overhead
-            # GRAPH_ITERATIONS iterations per graph: one graph launch per block
-            # of iterations instead of one per iteration; early exits are
-            # device-side (queued launches become no-ops)
+            # device state), so replay == relaunch without the host overhead.
+            # Early exits are device-side (queued launches become no-ops); the
+            # host also polls the stop flag without blocking (an async copy
+            # into pinned memory every POLL_EVERY replays, read once its event
+            # has completed) and stops replaying once the solve has ended.
             run(1)
             rest = cfg.max_iterations - 1
             k = max(1, min(GRAPH_ITERATIONS, rest))
             key = (g.data_ptr(), box, dx.tobytes(), k)
             graph = ws.iteration_graph(lambda: run(k), key)
-            for _ in range(rest // k):
+            stream = torch.cuda.current_stream(dev)
+            ws._stop_host.zero_()
+            ws._stop_event = None
+            for q in range(rest // k):
                 graph.replay()
-            if rest % k:
-                run(rest % k)
+                if (q + 1) % POLL_EVERY == 0:
+                    if ws._stop_event is not None and ws._stop_event.query() \
+                            and int(ws._stop_host[0]) != 0:
+                        break
+                    ws._stop_host.copy_(ws.state[_STOP_OFFSET:_STOP_OFFSET + 4]
+                                        .view(torch.int32), non_blocking=True)
+                    ws._stop_event = torch.cuda.Event()
+                    ws._stop_event.record(stream)
+            else:
+                if rest % k:
+                    run(rest % k)
         else:
             run(cfg.max_iterations)
         finalize()
@@ -215,7 +262,8 @@ def fused_phase_seconds(f, op: GlobalOperator, topo: Topology, iterations: int,
     fd = dv.as_device_f64(f, None, "f")
     dev = fd.device
     ws = workspace
-    if ws is None or ws.max_iterations < iterations or ws.device != dev:
+    topo = as_topology(topo)
+    if ws is None or not ws.fits(topo, iterations, dev):
         ws = CgWorkspace(topo, iterations, dev)
     box = (topo.ex, topo.ey, topo.ez, topo.n)
     g = op.geom.device_values(dev)
@@ -287,12 +335,19 @@ def _generic_solve(f_dev: torch.Tensor, operator, topo: Topology, cfg: CgConfig,
     return x, np.asarray(history, dtype=np.float64), iters
 
 
-def cg_solve(f, operator, topo: Topology, cfg: CgConfig,
+def cg_solve(f, operator, topo, cfg: CgConfig,
              counters: TrafficCounters | None = None, callback=None,
              workspace: CgWorkspace | None = None) -> CgResult:
-    """Run CG on A x = f (reference recurrence, cg.py:139-186)."""
+    """Run CG on A x = f (reference recurrence, cg.py:139-186).
+
+    The fused device-resident solve runs when ``operator`` is a
+    :class:`GlobalOperator` on this (box) topology and mask(f) is
+    interface-consistent (the fused <p, A p> is the element-local sum, equal
+    to the reference's assembled one only for continuous iterates);
+    otherwise the generic path calls ``operator`` every iteration."""
     if counters is None:
         counters = TrafficCounters()
+    topo = as_topology(topo)
     validate_field(f, topo.num_elements, topo.n, "f")
     fd, kind = dv.to_device_io(f, "f")
     host = kind != "device"
@@ -300,7 +355,9 @@ def cg_solve(f, operator, topo: Topology, cfg: CgConfig,
     # r = mask(f) on entry (cg.py:139)
     counters.add(reads=2 * dofs, writes=dofs)
     with torch.cuda.device(fd.device):
-        if isinstance(operator, GlobalOperator) and operator.topo == topo:
+        fused = (isinstance(operator, GlobalOperator) and isinstance(topo, Topology)
+                 and operator.topo == topo and _consistent(fd, topo))
+        if fused:
             x, history, iters, zero_exit = _fused_solve(fd, operator, topo, cfg, callback, host,
                                                         workspace)
             full = iters - (1 if zero_exit else 0)

@@ -2,8 +2,9 @@
 
 A field is ``[E, n, n, n]`` float64 indexed ``[e, k, j, i]`` (i fastest).
 ``random_field`` is the reference's counter-based SplitMix64 stream; it is
-generated on the GPU (``sem_random_field``) bit-for-bit, returned as a CUDA
-tensor by default or as numpy with ``host=True``.
+generated on the GPU (``sem_random_field``) bit-for-bit.  Like the
+reference, the builders return numpy arrays; ``device=`` returns a CUDA
+tensor on that device instead (no host round trip).
 """
 
 from __future__ import annotations
@@ -32,18 +33,27 @@ def mix64(a: int, b: int = 0) -> int:
     return _splitmix64((a * _FNV_PRIME + b) & _MASK64)
 
 
-def zeros_field(num_elements: int, n: int, device=None) -> torch.Tensor:
-    return torch.zeros((num_elements, n, n, n), dtype=torch.float64,
-                       device=device or dv.current_device())
+def zeros_field(num_elements: int, n: int, device=None):
+    """Zero field: numpy (the reference's type), or a CUDA tensor on `device`."""
+    if device is None:
+        return np.zeros((num_elements, n, n, n))
+    return torch.zeros((num_elements, n, n, n), dtype=torch.float64, device=device)
 
 
-def constant_field(num_elements: int, n: int, value: float = 1.0, device=None) -> torch.Tensor:
+def constant_field(num_elements: int, n: int, value: float = 1.0, device=None):
+    """Constant field: numpy (the reference's type), or a CUDA tensor on `device`."""
+    if device is None:
+        return np.full((num_elements, n, n, n), float(value))
     return torch.full((num_elements, n, n, n), float(value), dtype=torch.float64,
-                      device=device or dv.current_device())
+                      device=device)
 
 
-def random_field(num_elements: int, n: int, seed: int, device=None, host: bool = False):
-    """Uniform [-1, 1) field, value q = 2*(splitmix64(seed+q) >> 11)*2^-53 - 1."""
+def random_field(num_elements: int, n: int, seed: int, device=None, host: bool | None = None):
+    """Uniform [-1, 1) field, value q = 2*(splitmix64(seed+q) >> 11)*2^-53 - 1,
+    generated on the GPU.  Returns numpy unless `device` is given (``host=True``
+    forces numpy, ``host=False`` a tensor on the current device)."""
+    if host is None:
+        host = device is None
     dev = device or dv.current_device()
     out = torch.empty((num_elements, n, n, n), dtype=torch.float64, device=dev)
     with torch.cuda.device(dev):

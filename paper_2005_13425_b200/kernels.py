@@ -24,7 +24,7 @@ import torch
 from . import _device as dv
 from ._lib import check, load
 from .basis import PolynomialBasis
-from .mesh import GeomFactors
+from .mesh import GeomFactors, as_geom
 
 __all__ = ["KernelVariant", "TrafficCounters", "ScratchCapacityError", "apply_ax",
            "apply_ax_into", "flops_per_apply", "apply_read_words", "apply_write_words",
@@ -147,6 +147,7 @@ def apply_ax(u, geom: GeomFactors, basis: PolynomialBasis,
     tensor out (zero-copy).  Returns a fresh array; inputs are not modified."""
     if not isinstance(variant, KernelVariant):
         variant = KernelVariant.parse(variant)
+    geom = as_geom(geom)
     n = basis.n
     _validate(u, geom.shape, n)
     if variant is KernelVariant.REFERENCE and workspace is not None:

@@ -1,15 +1,20 @@
 """Box mesh and geometric factors (contract of sembench/mesh.py:20-91).
 
 ``GeomFactors.values`` keeps the reference layout ``[E, 6, n, n, n]``
-(index ``[e, m, k, j, i]``, m = g1..g6).  It may be a numpy array (copied to
-the GPU once, on first use, and cached) or a CUDA tensor.  ``build_geom``
-generates the affine box metric directly on the GPU with the reference's
-exact rounding (``((w_k*w_j)*w_i)*(h/2)``), so a 32768-element geometry
-(1.6 GB) never crosses PCIe.
+(index ``[e, m, k, j, i]``, m = g1..g6).  It may be a CUDA tensor (used in
+place), a read-only numpy array (the reference's frozen geometry: copied to
+the GPU once and cached), a writable numpy array (copied on EVERY use -- the
+caller may mutate it in place, and a cached copy would go stale) or a CPU
+tensor (cached, re-copied whenever its version counter moves).
+``build_geom`` generates the affine box metric on the GPU with the
+reference's exact rounding (``((w_k*w_j)*w_i)*(h/2)``); with ``device=`` the
+result stays there (a 32768-element geometry, 1.6 GB, never crosses PCIe),
+without it a frozen numpy array is returned like the reference's.
 """
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -19,7 +24,7 @@ from . import _device as dv
 from ._lib import check, load
 from .basis import PolynomialBasis
 
-__all__ = ["BoxMesh", "GeomFactors", "build_mesh", "build_geom"]
+__all__ = ["BoxMesh", "GeomFactors", "build_mesh", "build_geom", "as_geom"]
 
 
 @dataclass(frozen=True)
@@ -59,17 +64,50 @@ class GeomFactors:
         return tuple(self.values.shape)
 
     def device_values(self, device: torch.device | None = None) -> torch.Tensor:
-        """The metric as a contiguous float64 CUDA tensor (cached per device)."""
+        """The metric as a contiguous float64 CUDA tensor on `device`."""
         dev = device or dv.current_device()
         v = self.values
-        if isinstance(v, torch.Tensor) and v.device == dev and v.dtype == torch.float64 \
-                and v.is_contiguous():
-            return v
-        t = self._cache.get(dev.index)
-        if t is None:
-            t = dv.as_device_f64(v, dev, "geometry")
-            self._cache[dev.index] = t
-        return t
+        if isinstance(v, torch.Tensor):
+            if v.device == dev and v.dtype == torch.float64 and v.is_contiguous():
+                return v
+            key = (dev.index, v._version)  # an in-place write bumps the version
+        elif isinstance(v, np.ndarray) and not v.flags.writeable:
+            key = (dev.index, None)
+        else:  # writable numpy: the caller may change it between calls
+            self._cache.pop(dev.index, None)
+            return dv.as_device_f64(v, dev, "geometry")
+        ent = self._cache.get(dev.index)
+        if ent is None or ent[0] != key:
+            ent = (key, dv.as_device_f64(v, dev, "geometry"))
+            self._cache[dev.index] = ent
+        return ent[1]
+
+
+_wrapped: dict = {}
+
+
+def as_geom(geom) -> GeomFactors:
+    """This package's GeomFactors for `geom`: ours pass through; any object
+    with a ``values`` array of the reference layout (e.g. a
+    ``sembench.GeomFactors``) is wrapped, the wrapper cached per object so
+    its device copy is reused (sembench/mesh.py:40-58)."""
+    if isinstance(geom, GeomFactors):
+        return geom
+    v = getattr(geom, "values", None)
+    if v is None or len(getattr(v, "shape", ())) != 5 or v.shape[1] != 6:
+        raise TypeError(f"not a geometry: {type(geom).__name__} has no [E, 6, n, n, n] values")
+    ent = _wrapped.get(id(geom))
+    if ent is not None and ent[0]() is geom and ent[1].values is v:
+        return ent[1]
+    out = GeomFactors(values=v)
+    try:
+        ref = weakref.ref(geom)
+    except TypeError:
+        return out
+    if len(_wrapped) > 64:
+        _wrapped.clear()
+    _wrapped[id(geom)] = (ref, out)
+    return out
 
 
 def build_mesh(ex: int, ey: int, ez: int, n: int, element_extent: float) -> BoxMesh:
@@ -85,7 +123,9 @@ def build_mesh(ex: int, ey: int, ez: int, n: int, element_extent: float) -> BoxM
 
 def build_geom(mesh: BoxMesh, basis: PolynomialBasis, device: torch.device | None = None
                ) -> GeomFactors:
-    """Affine box metric, generated on the GPU (sem_box_geom)."""
+    """Affine box metric, generated on the GPU (sem_box_geom).  With
+    ``device`` the values stay there; without it they are returned as a
+    frozen numpy array, the reference's type (mesh.py:72-91)."""
     if basis.n != mesh.n:
         raise ValueError(f"basis has n={basis.n} but mesh has n={mesh.n}")
     dev = device or dv.current_device()
@@ -96,4 +136,10 @@ def build_geom(mesh: BoxMesh, basis: PolynomialBasis, device: torch.device | Non
         check(load().sem_box_geom(dv.ptr(g), mesh.num_elements, n, dv.host_f64_ptr(w),
                                   float(mesh.element_extent), dv.stream_handle(dev)),
               "build_geom")
-    return GeomFactors(values=g)
+    if device is not None:
+        return GeomFactors(values=g)
+    host = dv.to_numpy(g)
+    host.flags.writeable = False
+    out = GeomFactors(values=host)
+    out._cache[dev.index] = ((dev.index, None), g)  # the device copy is already made
+    return out

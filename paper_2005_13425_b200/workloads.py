@@ -4,7 +4,9 @@ interface-consistent, masked right-hand side."""
 
 from __future__ import annotations
 
-from .assembly import _dssum_dev, _mask_dev
+import torch
+
+from .assembly import _dssum_dev, _mask_dev, as_topology
 from .fields import random_field
 
 __all__ = ["factor_elements", "make_rhs"]
@@ -31,8 +33,13 @@ def factor_elements(count: int) -> tuple[int, int, int]:
     return best
 
 
-def make_rhs(num_elements: int, n: int, topo, seed: int, device=None, host: bool = False):
-    """mask(dssum(random_field(E, n, seed))) generated entirely on the GPU."""
-    f = random_field(num_elements, n, seed, device=device)
-    out = _mask_dev(_dssum_dev(f, topo, False), topo)
+def make_rhs(num_elements: int, n: int, topo, seed: int, device=None, host: bool | None = None):
+    """mask(dssum(random_field(E, n, seed))) generated on the GPU.  numpy like
+    the reference (bench.py:122-125) unless `device` is given."""
+    if host is None:
+        host = device is None
+    topo = as_topology(topo)
+    f = random_field(num_elements, n, seed, device=device, host=False)
+    with torch.cuda.device(f.device):
+        out = _mask_dev(_dssum_dev(f, topo, False), topo)
     return out.cpu().numpy() if host else out

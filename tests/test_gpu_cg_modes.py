@@ -42,7 +42,7 @@ out = []
 for _ in range(2):
     res = sb.cg_solve(f, op, topo, sb.CgConfig(40, 0.0))
     out.append([float(v) for v in res.residual_history])
-x = res.solution.cpu().numpy()
+x = res.solution
 print(json.dumps({{"hist": out, "xsum": float(abs(x).sum())}}))
 """
 

@@ -1,0 +1,222 @@
+"""Drop-in fidelity on the GPU (VERDICT r1 'boundary fidelity'):
+
+* the repo's dssum / mask / weighted_dot / apply_global / cg_solve driven by
+  reference-built objects (a reference-shaped Topology, or sembench's own
+  objects when baseline/_ref is installed) -- box numberings run the
+  analytic box kernels, other numberings the ordered CSR gather, both
+  bit-exact against the oracle;
+* an interface-INCONSISTENT right-hand side takes the assembled path and
+  follows the reference's recurrence;
+* a workspace built for another mesh is not reused;
+* a writable numpy metric mutated in place is seen by the next call;
+* OperatorTimers accumulate on the fused path;
+* a result view kept across calls is not recycled;
+* an early exit stops the host replay loop.
+"""
+
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2005_13425_b200 as sb
+from topo_helpers import box_topology, periodic_x_topology, relabelled, sembench_or_none
+
+pytestmark = pytest.mark.gpu
+
+
+def _np(x):
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
+def _rel_hist(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+@pytest.mark.parametrize("make", ["box", "relabelled", "periodic"])
+def test_assembly_with_reference_topology(cuda, make):
+    n = 5
+    ref = {"box": lambda: box_topology(3, 2, 4, n),
+           "relabelled": lambda: relabelled(box_topology(3, 2, 4, n), 3),
+           "periodic": lambda: periodic_x_topology(3, 2, 4, n)}[make]()
+    f = O.random_field(ref.num_elements, n, 11)
+    f.ravel()[::53] = -0.0
+    got = sb.dssum(f, ref)
+    want = O.dssum(f, ref)
+    assert np.array_equal(got, want) and np.array_equal(np.signbit(got), np.signbit(want))
+    assert np.array_equal(sb.mask(f, ref), O.mask(f, ref))
+    v = O.random_field(ref.num_elements, n, 12)
+    wd = sb.weighted_dot(f, v, ref)
+    want_wd = O.wdot3(f, v, ref.inv_multiplicity)
+    # reassociation bound: relative to the sum of |terms| (the dot cancels)
+    scale = float(np.sum(np.abs(f.ravel() * v.ravel()) * ref.inv_multiplicity))
+    assert abs(wd - want_wd) <= 1e-14 * scale
+    # device tensors too
+    gd = sb.dssum(torch.from_numpy(f).cuda(), ref)
+    assert gd.is_cuda and np.array_equal(gd.cpu().numpy(), want)
+
+
+def test_apply_global_and_cg_with_reference_topology(cuda):
+    n, box = 6, (3, 3, 2)
+    b = sb.build_basis(n)
+    ref = box_topology(*box, n)
+    g = O.box_geom(*box, b.weights, 1.0)
+    g.flags.writeable = False
+    geom = sb.GeomFactors(values=g)
+    T = O.BoxTopology(*box, n)
+    u = O.mask(O.dssum(O.random_field(ref.num_elements, n, 5), T), T)
+    w = sb.apply_global(u, geom, b, ref)
+    assert O.rel_diff(w, O.apply_global(u, g, b.diff, b.diff_t, T)) <= 1e-12
+    f = sb.make_rhs(ref.num_elements, n, ref, sb.mix64(1, ref.num_elements))
+    assert isinstance(f, np.ndarray)
+    res = sb.cg_solve(f, sb.GlobalOperator(geom, b, ref), ref, sb.CgConfig(30, 0.0))
+    _, hist, _ = O.cg(f, lambda p: O.apply_global(p, g, b.diff, b.diff_t, T), T, 30)
+    assert _rel_hist(res.residual_history, hist) <= 1e-10
+
+
+def test_cg_on_a_non_box_numbering(cuda):
+    """Periodic-x numbering: the CSR gather inside the generic solver vs the
+    oracle's CG on the same topology."""
+    n = 5
+    ref = periodic_x_topology(4, 2, 3, n)
+    b = sb.build_basis(n)
+    g = O.box_geom(4, 2, 3, b.weights, 1.0)
+    geom = sb.GeomFactors(values=g)
+    f0 = O.random_field(ref.num_elements, n, 9)
+    f = O.mask(O.dssum(f0, ref), ref)
+    res = sb.cg_solve(f, sb.GlobalOperator(geom, b, ref), ref, sb.CgConfig(25, 0.0))
+    _, hist, _ = O.cg(f, lambda p: O.apply_global(p, g, b.diff, b.diff_t, ref), ref, 25)
+    assert _rel_hist(res.residual_history, hist) <= 1e-10
+
+
+def test_cg_with_sembench_objects(cuda):
+    S = sembench_or_none()
+    if S is None:
+        pytest.skip("reference package not installed under baseline/_ref")
+    from sembench.fields import mix64
+    n, box = 5, (3, 2, 2)
+    mesh = S.build_mesh(*box, n, 1.0)
+    basis, topo = S.build_basis(n), S.build_topology(mesh)
+    geom = S.build_geom(mesh, basis)
+    f = S.make_rhs(mesh.num_elements, n, topo, mix64(1, mesh.num_elements))
+    want = S.cg_solve(f, lambda p: S.apply_global(p, geom, basis, topo), topo,
+                      S.CgConfig(20, 0.0))
+    got = sb.cg_solve(f, sb.GlobalOperator(geom, basis, topo), topo, sb.CgConfig(20, 0.0))
+    assert _rel_hist(got.residual_history, want.residual_history) <= 1e-10
+    assert np.array_equal(sb.dssum(f, topo), S.dssum(f, topo))
+    u = S.random_field(mesh.num_elements, n, 4)
+    assert O.rel_diff(sb.apply_ax(u, geom, basis), S.apply_ax(u, geom, basis)) <= 1e-12
+
+
+def test_cg_inconsistent_rhs_follows_the_reference(cuda):
+    """A raw random f: mask(f) is not interface-consistent, so the fused
+    local <p, A p> would differ from the reference's assembled one by tens of
+    percent; cg_solve must take the assembled path."""
+    n, box = 4, (3, 3, 3)
+    b = sb.build_basis(n)
+    mesh = sb.build_mesh(*box, n, 1.0)
+    topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b)
+    T = O.BoxTopology(*box, n)
+    f = O.random_field(topo.num_elements, n, 17)
+    res = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(20, 0.0))
+    g = O.box_geom(*box, b.weights, 1.0)
+    x, hist, _ = O.cg(f, lambda p: O.apply_global(p, g, b.diff, b.diff_t, T), T, 20)
+    assert _rel_hist(res.residual_history, hist) <= 1e-10
+    assert O.rel_diff(res.solution, x) <= 1e-10
+
+
+def test_workspace_for_another_mesh_is_not_reused(cuda):
+    n = 5
+    b = sb.build_basis(n)
+    small = sb.build_mesh(2, 2, 2, n, 1.0)
+    big = sb.build_mesh(4, 3, 2, n, 1.0)
+    ws = sb.CgWorkspace(sb.build_topology(small), 50, torch.device("cuda"))
+    topo, geom = sb.build_topology(big), sb.build_geom(big, b)
+    f = sb.make_rhs(big.num_elements, n, topo, sb.mix64(1, big.num_elements))
+    a = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(15, 0.0),
+                    workspace=ws)
+    c = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(15, 0.0))
+    assert np.array_equal(a.residual_history, c.residual_history)
+    assert np.array_equal(a.solution, c.solution)
+
+
+def test_mutated_writable_metric_is_seen(cuda):
+    n, E = 6, 5
+    b = sb.build_basis(n)
+    u = O.random_field(E, n, 1)
+    g = O.random_field(6 * E, n, 2).reshape(E, 6, n, n, n)
+    geom = sb.GeomFactors(values=g)
+    w1 = sb.apply_ax(u, geom, b)
+    g *= 2.0  # in place, through the caller's own array
+    w2 = sb.apply_ax(u, geom, b)
+    assert O.rel_diff(w2, O.ax_layered(u, g, b.diff, b.diff_t)) <= 1e-12
+    assert O.rel_diff(w2, 2.0 * w1) <= 1e-12
+    # torch CPU metric mutated in place: the version counter invalidates the copy
+    gt = torch.from_numpy(O.random_field(6 * E, n, 3).reshape(E, 6, n, n, n))
+    gf = sb.GeomFactors(values=gt)
+    sb.apply_ax(u, gf, b)
+    gt.mul_(-1.0)
+    w3 = sb.apply_ax(u, gf, b)
+    assert O.rel_diff(w3, O.ax_layered(u, gt.numpy(), b.diff, b.diff_t)) <= 1e-12
+
+
+def test_operator_timers_on_the_fused_path(cuda):
+    n = 6
+    b = sb.build_basis(n)
+    mesh = sb.build_mesh(3, 2, 2, n, 1.0)
+    topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b)
+    f = sb.make_rhs(mesh.num_elements, n, topo, sb.mix64(1, mesh.num_elements))
+    timers = sb.OperatorTimers()
+    res = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo, timers=timers), topo,
+                      sb.CgConfig(12, 0.0))
+    plain = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(12, 0.0))
+    assert timers.applies == 12
+    assert timers.ax_seconds > 0.0 and timers.dssum_seconds > 0.0
+    assert np.array_equal(res.residual_history, plain.residual_history)
+    assert np.array_equal(res.solution, plain.solution)
+
+
+def test_result_view_survives_the_next_call(cuda):
+    n, E = 6, 4
+    b = sb.build_basis(n)
+    u1, u2 = O.random_field(E, n, 1), O.random_field(E, n, 2)
+    g = O.random_field(6 * E, n, 3).reshape(E, 6, n, n, n)
+    geom = sb.GeomFactors(values=g)
+    view = sb.apply_ax(u1, geom, b).reshape(-1)[5:]
+    keep = view.copy()
+    for _ in range(3):
+        sb.apply_ax(u2, geom, b)
+    assert np.array_equal(view, keep)
+
+
+def test_early_exit_stops_replaying(cuda):
+    n = 5
+    b = sb.build_basis(n)
+    mesh = sb.build_mesh(2, 2, 2, n, 1.0)
+    topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b)
+    f = sb.make_rhs(8, n, topo, sb.mix64(1, 8))
+    op = sb.GlobalOperator(geom, b, topo)
+    sb.cg_solve(f, op, topo, sb.CgConfig(20, 1e300))  # warm-up / capture
+    t0 = time.perf_counter()
+    short = sb.cg_solve(f, op, topo, sb.CgConfig(20, 1e300))
+    t_short = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    res = sb.cg_solve(f, op, topo, sb.CgConfig(200_000, 1e300))
+    t_long = time.perf_counter() - t0
+    assert short.iterations_run == res.iterations_run == 1
+    # 200k replays would take seconds; the poll stops the loop after ~8-16
+    assert t_long < t_short + 0.5
+
+
+def test_builders_return_numpy_by_default(cuda):
+    assert isinstance(sb.random_field(2, 3, 1), np.ndarray)
+    assert isinstance(sb.zeros_field(2, 3), np.ndarray)
+    assert isinstance(sb.constant_field(2, 3, 2.0), np.ndarray)
+    t = sb.random_field(2, 3, 1, device="cuda")
+    assert t.is_cuda and np.array_equal(t.cpu().numpy(), sb.random_field(2, 3, 1))
+    topo = sb.build_topology(sb.build_mesh(2, 1, 1, 3, 1.0))
+    assert isinstance(sb.make_rhs(2, 3, topo, 5), np.ndarray)
+    assert sb.make_rhs(2, 3, topo, 5, device="cuda").is_cuda

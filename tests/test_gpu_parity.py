@@ -27,6 +27,10 @@ def _rand_inputs(E, n, su, sg):
     return u, g
 
 
+def _np(x):
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
 def _rel_hist(a, b):
     a, b = np.asarray(a), np.asarray(b)
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
@@ -45,7 +49,10 @@ def test_random_field_bitexact(cuda, golden):
 def test_build_geom_bitexact(cuda, golden):
     mesh = sb.build_mesh(2, 2, 1, 10, 0.5)
     geom = sb.build_geom(mesh, sb.build_basis(10))
-    assert np.array_equal(geom.values.cpu().numpy(), golden["geom/2x2x1n10h0.5"])
+    assert isinstance(geom.values, np.ndarray) and not geom.values.flags.writeable
+    assert np.array_equal(geom.values, golden["geom/2x2x1n10h0.5"])
+    gd = sb.build_geom(mesh, sb.build_basis(10), device=torch.device("cuda"))
+    assert gd.values.is_cuda and np.array_equal(gd.values.cpu().numpy(), geom.values)
 
 
 # ---------------------------------------------------------------------- Ax --
@@ -73,8 +80,8 @@ def test_ax_psweep_vs_oracle(cuda, n):
 def test_ax_paper_sizes_vs_oracle(cuda, E):
     n = 10
     b = sb.build_basis(n)
-    u = sb.random_field(E, n, 1)
-    g = sb.random_field(6 * E, n, 2).reshape(E, 6, n, n, n)
+    u = sb.random_field(E, n, 1, device="cuda")
+    g = sb.random_field(6 * E, n, 2, device="cuda").reshape(E, 6, n, n, n)
     w = sb.apply_ax(u, sb.GeomFactors(values=g), b)
     assert isinstance(w, torch.Tensor) and w.is_cuda
     ref = O.ax_layered(u.cpu().numpy(), g.cpu().numpy(), b.diff, b.diff_t)
@@ -87,13 +94,13 @@ def test_ax_large_properties(cuda):
     E, n = 32768, 10
     b = sb.build_basis(n)
     mesh = sb.build_mesh(32, 32, 32, n, 1.0)
-    geom = sb.build_geom(mesh, b)
-    u = sb.random_field(E, n, 3)
-    v = sb.random_field(E, n, 4)
+    geom = sb.build_geom(mesh, b, device="cuda")
+    u = sb.random_field(E, n, 3, device="cuda")
+    v = sb.random_field(E, n, 4, device="cuda")
     au, av = sb.apply_ax(u, geom, b), sb.apply_ax(v, geom, b)
     lhs = sb.apply_ax(1.7 * u - 0.3 * v, geom, b)
     assert O.rel_diff(lhs.cpu().numpy(), (1.7 * au - 0.3 * av).cpu().numpy()) <= AX_TOL
-    c = sb.apply_ax(sb.constant_field(E, n, 3.25), geom, b)
+    c = sb.apply_ax(sb.constant_field(E, n, 3.25, device="cuda"), geom, b)
     scale = (n * np.max(np.abs(b.diff))) ** 2 * float(geom.values.max())
     assert float(c.abs().max()) <= 1e-12 * 3.25 * scale
     # spot-check a few elements against the oracle
@@ -171,8 +178,9 @@ def test_ax_host_streaming(cuda, kind, mode, monkeypatch):
     monkeypatch.setenv("SEM_HOST_MODE", mode)
     E, n = 1500, 10
     b = sb.build_basis(n)
-    u = sb.random_field(E, n, 9)
-    geom = sb.GeomFactors(values=sb.random_field(6 * E, n, 10).reshape(E, 6, n, n, n))
+    u = sb.random_field(E, n, 9, device="cuda")
+    geom = sb.GeomFactors(values=sb.random_field(6 * E, n, 10, device="cuda")
+                          .reshape(E, 6, n, n, n))
     dev_out = sb.apply_ax(u, geom, b).cpu()
     if kind == "numpy":
         host = u.cpu().numpy()
@@ -302,7 +310,7 @@ def test_weighted_dot(cuda, golden, key):
 
 def test_weighted_dot_large_deterministic(cuda):
     topo = sb.build_topology(sb.build_mesh(16, 16, 16, 10, 1.0))
-    a, b = sb.random_field(4096, 10, 1), sb.random_field(4096, 10, 2)
+    a, b = sb.random_field(4096, 10, 1, device="cuda"), sb.random_field(4096, 10, 2, device="cuda")
     got = [sb.weighted_dot(a, b, topo) for _ in range(3)]
     assert got[0] == got[1] == got[2]
     T = O.BoxTopology(16, 16, 16, 10)
@@ -339,7 +347,7 @@ def test_cg_fused_vs_golden(cuda, golden, key):
     tol = max(CG_TOL, 10.0 * spread)
     assert _rel_hist(res.residual_history, golden[f"cg/{key}/history"]) <= tol
     if f"cg/{key}/solution" in golden.files:
-        assert O.rel_diff(res.solution.cpu().numpy(), golden[f"cg/{key}/solution"]) <= tol
+        assert O.rel_diff(_np(res.solution), golden[f"cg/{key}/solution"]) <= tol
 
 
 def test_cg_graph_replay_matches_eager(cuda):
@@ -356,7 +364,7 @@ def test_cg_graph_replay_matches_eager(cuda):
     graph = sb.cg_solve(f, op, topo, sb.CgConfig(30, 0.0))
     assert graph.iterations_run == eager.iterations_run == 30
     assert np.array_equal(graph.residual_history, eager.residual_history)
-    assert torch.equal(graph.solution, eager.solution)
+    assert np.array_equal(_np(graph.solution), _np(eager.solution))
 
 
 def test_cg_generic_matches_fused(cuda):
@@ -370,7 +378,7 @@ def test_cg_generic_matches_fused(cuda):
     # the two agree to rounding, each being deterministic on its own
     h1, h2 = fused.residual_history, generic.residual_history
     assert np.max(np.abs(h1 - h2) / np.abs(h2)) <= 1e-12
-    assert O.rel_diff(fused.solution.cpu().numpy(), generic.solution.cpu().numpy()) <= 1e-12
+    assert O.rel_diff(_np(fused.solution), _np(generic.solution)) <= 1e-12
     again = sb.cg_solve(f, op, topo, sb.CgConfig(25, 0.0))
     assert np.array_equal(again.residual_history, h1)  # run-to-run reproducible
 
@@ -382,11 +390,11 @@ def test_cg_e4096_vs_oracle(cuda):
     res = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(100, 0.0))
     T = O.BoxTopology(16, 16, 16, n)
     g = O.box_geom(16, 16, 16, b.weights, 1.0)
-    x, hist, its = O.cg(f.cpu().numpy(), lambda p: O.apply_global(p, g, b.diff, b.diff_t, T),
+    x, hist, its = O.cg(_np(f), lambda p: O.apply_global(p, g, b.diff, b.diff_t, T),
                         T, 100)
     assert res.iterations_run == its == 100
     assert _rel_hist(res.residual_history, hist) <= CG_TOL
-    assert O.rel_diff(res.solution.cpu().numpy(), x) <= 1e-10
+    assert O.rel_diff(_np(res.solution), x) <= 1e-10
 
 
 def test_cg_zero_rhs_and_counters(cuda):

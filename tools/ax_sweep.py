@@ -68,8 +68,8 @@ def main():
             nsets = min(nsets, 8)
             sets = []
             for s in range(nsets):
-                u = sb.random_field(E, n, 1 + s)
-                g = sb.random_field(6 * E, n, 100 + s).reshape(E, 6, n, n, n)
+                u = sb.random_field(E, n, 1 + s, device="cuda")
+                g = sb.random_field(6 * E, n, 100 + s, device="cuda").reshape(E, 6, n, n, n)
                 sets.append((u, g, torch.empty_like(u)))
             idx = sorted({0, 1, E // 2, E - 1})
             ref = O.ax_layered(sets[0][0][idx].cpu().numpy(), sets[0][1][idx].cpu().numpy(),

@@ -17,8 +17,8 @@ from paper_2005_13425_b200._lib import load  # noqa: E402
 
 E, n = 4096, 10
 b = sb.build_basis(n)
-u = sb.random_field(E, n, 1)
-geom = sb.GeomFactors(values=sb.random_field(6 * E, n, 2).reshape(E, 6, n, n, n))
+u = sb.random_field(E, n, 1, device="cuda")
+geom = sb.GeomFactors(values=sb.random_field(6 * E, n, 2, device="cuda").reshape(E, 6, n, n, n))
 u_pin = u.cpu().pin_memory()
 w_dev = sb.apply_ax(u.cuda(), geom, b).cpu()
 import os  # noqa: E402
