@@ -33,6 +33,7 @@
 #include "sem_common.cuh"
 #include "ax_pencil.cuh"
 #include "ax_half.cuh"
+#include "ax_split.cuh"
 #include "box.cuh"
 
 namespace sem {
@@ -386,6 +387,11 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     static const char* pf_env = getenv("SEM_AX_PFDIST");  // tuning probe
     if (pf_env) pf = atoll(pf_env);
     if (cgp.grid_out) *cgp.grid_out = (unsigned)grid;
+    // plain Ax as a programmatic dependent (CGM == 0): the pre-wait L2
+    // prefetch of the CTA's own blocks (pdl == 2) pays for short launches and
+    // cost ~0.6% on long ones (E = 1024: 13.2 -> 12.9 us; E = 4096: 41.7 ->
+    // 41.9 us; profiles/r02_ax_pdl_ab.txt), so it is kept below ~200 MB
+    if (CGM == 0 && cgp.pdl == 2 && E * (int64_t)C::NNN * 64 > (int64_t)200e6) cgp.pdl = 1;
     if (cgp.pdl) {
         cudaError_t err = launch_k(kern, dim3((unsigned)grid), dim3(THREADS), SMEM, stream, true,
                                    u, g, w, E, D, pf, cgp);
@@ -455,6 +461,46 @@ static int launch_half(const double* u, const double* g, const double* dx, doubl
     }
 }
 
+// Split-element kernel (ax_split.cuh): the two k-halves of an element on a
+// 2-CTA cluster.
+template <int N, int MINB, int GM, bool FOLD, bool ALIAS>
+static int launch_split(const double* u, const double* g, const double* dx, double* w, int64_t E,
+                        cudaStream_t stream, int pdl)
+{
+    using C = SplitCfg<N, ALIAS>;
+    constexpr size_t SMEM = C::template smem<GM>();
+    if constexpr (C::THREADS > 1024 || (SMEM + 1024) * MINB > 228 * 1024 || (GM && N % 2 != 0)) {
+        note_fallback();
+        return try_pencil<N, PencilCfg<N>::SLOTS, 1, false>(u, g, dx, w, E, stream);
+    } else {
+        DParamP<N> D;
+        const bool antisym = fill_dparam<N>(D, dx);
+        if constexpr (FOLD) {
+            if (!antisym) return launch_split<N, MINB, GM, false, ALIAS>(u, g, dx, w, E, stream, pdl);
+        }
+        if (E == 0) return 0;
+        if (E > 0x3fffffffLL) {
+            set_error("sem_ax: too many elements (%lld)", (long long)E);
+            return SEM_E_INVALID;
+        }
+        auto kern = ax_split_kernel<N, MINB, GM, FOLD, ALIAS>;
+        static std::atomic<uint64_t> configured{0};
+        int dev = 0;
+        if (cudaError_t err = cudaGetDevice(&dev)) return fail_cuda(err, "sem_ax: cudaGetDevice");
+        const uint64_t bit = 1ull << (dev & 63);
+        if (!(configured.load(std::memory_order_acquire) & bit)) {
+            cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)SMEM);
+            if (err != cudaSuccess) return fail_cuda(err, "sem_ax: cudaFuncSetAttribute");
+            configured.fetch_or(bit, std::memory_order_release);
+        }
+        cudaError_t err = launch_k(kern, dim3((unsigned)(2 * E)), dim3(C::THREADS), SMEM, stream,
+                                   pdl != 0, u, g, w, E, D, pdl);
+        if (err != cudaSuccess) return fail_cuda(err, "sem_ax (split) launch");
+        return 0;
+    }
+}
+
 // variant 0: the tuned default for this n (kDefaultVariant);
 // 1: per-point layered kernel (first B200 version, kept for ablation);
 // 2..19: pencil tuning points <elements per CTA, CTAs per SM, metric
@@ -469,52 +515,57 @@ constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41,
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
-                int variant, cudaStream_t stream)
+                int variant, int pdl, cudaStream_t stream)
 {
     constexpr int S = PencilCfg<N>::SLOTS;
     if (variant == 0) variant = kDefaultVariant[N];
+    // pencil kernels launched as programmatic dependents: their CTAs wait
+    // (griddepcontrol.wait) for the predecessor at entry, so a grid can be
+    // resident while the previous kernel in the stream drains
+    CgpArgs pa{};
+    pa.pdl = pdl;
     switch (variant) {
-        case 19: return try_pencil<N, S, 1, false>(u, g, dx, w, E, stream);
-        case 20: return try_pencil<N, 1, 4, false, 3>(u, g, dx, w, E, stream);
-        case 21: return try_pencil<N, 1, 4, false, 4>(u, g, dx, w, E, stream);
-        case 22: return try_pencil<N, 1, 4, false, 5>(u, g, dx, w, E, stream);
-        case 23: return try_pencil<N, 1, 5, false, 2>(u, g, dx, w, E, stream);
-        case 24: return try_pencil<N, 1, 3, false, 5>(u, g, dx, w, E, stream);
-        case 25: return try_pencil<N, 1, 3, false, 1, false, 1>(u, g, dx, w, E, stream);
-        case 26: return try_pencil<N, 1, 2, false, 1, false, 1>(u, g, dx, w, E, stream);
-        case 27: return try_pencil<N, 1, 3, false, 1, false, 2>(u, g, dx, w, E, stream);
-        case 28: return try_pencil<N, 1, 4, false, 1, false, 1>(u, g, dx, w, E, stream);
-        case 29: return try_pencil<N, 1, 4, false, 1, false, 2>(u, g, dx, w, E, stream);
-        case 30: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 1>(u, g, dx, w, E, stream);
-        case 31: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream);
-        case 32: return try_pencil<N, (S + 2) / 3, 3, false, 1, false, 2>(u, g, dx, w, E, stream);
-        case 33: return try_pencil<N, 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream);
+        case 19: return try_pencil<N, S, 1, false>(u, g, dx, w, E, stream, pa);
+        case 20: return try_pencil<N, 1, 4, false, 3>(u, g, dx, w, E, stream, pa);
+        case 21: return try_pencil<N, 1, 4, false, 4>(u, g, dx, w, E, stream, pa);
+        case 22: return try_pencil<N, 1, 4, false, 5>(u, g, dx, w, E, stream, pa);
+        case 23: return try_pencil<N, 1, 5, false, 2>(u, g, dx, w, E, stream, pa);
+        case 24: return try_pencil<N, 1, 3, false, 5>(u, g, dx, w, E, stream, pa);
+        case 25: return try_pencil<N, 1, 3, false, 1, false, 1>(u, g, dx, w, E, stream, pa);
+        case 26: return try_pencil<N, 1, 2, false, 1, false, 1>(u, g, dx, w, E, stream, pa);
+        case 27: return try_pencil<N, 1, 3, false, 1, false, 2>(u, g, dx, w, E, stream, pa);
+        case 28: return try_pencil<N, 1, 4, false, 1, false, 1>(u, g, dx, w, E, stream, pa);
+        case 29: return try_pencil<N, 1, 4, false, 1, false, 2>(u, g, dx, w, E, stream, pa);
+        case 30: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 1>(u, g, dx, w, E, stream, pa);
+        case 31: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream, pa);
+        case 32: return try_pencil<N, (S + 2) / 3, 3, false, 1, false, 2>(u, g, dx, w, E, stream, pa);
+        case 33: return try_pencil<N, 2, 2, false, 1, false, 2>(u, g, dx, w, E, stream, pa);
         // even-odd folded contractions (centro-antisymmetric D only)
-        case 34: return try_pencil<N, 1, 3, false, 1, false, 1, true>(u, g, dx, w, E, stream);
-        case 35: return try_pencil<N, 1, 2, false, 1, false, 1, true>(u, g, dx, w, E, stream);
-        case 36: return try_pencil<N, 1, 5, false, 3, false, 0, true>(u, g, dx, w, E, stream);
-        case 37: return try_pencil<N, 1, 4, false, 1, false, 1, true>(u, g, dx, w, E, stream);
-        case 38: return try_pencil<N, 1, 3, false, 1, false, 2, true>(u, g, dx, w, E, stream);
-        case 39: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 1, true>(u, g, dx, w, E, stream);
+        case 34: return try_pencil<N, 1, 3, false, 1, false, 1, true>(u, g, dx, w, E, stream, pa);
+        case 35: return try_pencil<N, 1, 2, false, 1, false, 1, true>(u, g, dx, w, E, stream, pa);
+        case 36: return try_pencil<N, 1, 5, false, 3, false, 0, true>(u, g, dx, w, E, stream, pa);
+        case 37: return try_pencil<N, 1, 4, false, 1, false, 1, true>(u, g, dx, w, E, stream, pa);
+        case 38: return try_pencil<N, 1, 3, false, 1, false, 2, true>(u, g, dx, w, E, stream, pa);
+        case 39: return try_pencil<N, (S + 1) / 2, 2, false, 1, false, 1, true>(u, g, dx, w, E, stream, pa);
         // + bulk L2 prefetch of the element a resident wave ahead
-        case 40: return try_pencil<N, 1, 3, false, 1, true, 1, true>(u, g, dx, w, E, stream);
-        case 41: return try_pencil<N, 1, 2, false, 1, true, 1, true>(u, g, dx, w, E, stream);
+        case 40: return try_pencil<N, 1, 3, false, 1, true, 1, true>(u, g, dx, w, E, stream, pa);
+        case 41: return try_pencil<N, 1, 2, false, 1, true, 1, true>(u, g, dx, w, E, stream, pa);
         // large n: folded contractions with the metric register ring
-        case 42: return try_pencil<N, 1, 2, false, 1, false, 0, true>(u, g, dx, w, E, stream);
-        case 43: return try_pencil<N, 1, 2, false, 2, false, 0, true>(u, g, dx, w, E, stream);
-        case 44: return try_pencil<N, 1, 2, false, 1, true, 0, true>(u, g, dx, w, E, stream);
-        case 45: return try_pencil<N, 1, 3, false, 1, false, 0, true>(u, g, dx, w, E, stream);
-        case 46: return try_pencil<N, 1, 1, false, 2, false, 0, true>(u, g, dx, w, E, stream);
+        case 42: return try_pencil<N, 1, 2, false, 1, false, 0, true>(u, g, dx, w, E, stream, pa);
+        case 43: return try_pencil<N, 1, 2, false, 2, false, 0, true>(u, g, dx, w, E, stream, pa);
+        case 44: return try_pencil<N, 1, 2, false, 1, true, 0, true>(u, g, dx, w, E, stream, pa);
+        case 45: return try_pencil<N, 1, 3, false, 1, false, 0, true>(u, g, dx, w, E, stream, pa);
+        case 46: return try_pencil<N, 1, 1, false, 2, false, 0, true>(u, g, dx, w, E, stream, pa);
         // large n: register ring + the CTA's own element bulk-prefetched to L2
-        case 47: return try_pencil<N, 1, 2, false, 1, 2, 0, true>(u, g, dx, w, E, stream);
-        case 48: return try_pencil<N, 1, 2, false, 2, 2, 0, true>(u, g, dx, w, E, stream);
-        case 49: return try_pencil<N, 1, 2, false, 1, 2, 0, false>(u, g, dx, w, E, stream);
-        case 50: return try_pencil<N, 1, 3, false, 1, 2, 0, true>(u, g, dx, w, E, stream);
-        case 51: return try_pencil<N, 1, 1, false, 3, 2, 0, true>(u, g, dx, w, E, stream);
-        case 52: return try_pencil<N, 1, 3, false, 1, 2, 1, true>(u, g, dx, w, E, stream);
-        case 53: return try_pencil<N, 1, 2, false, 1, 2, 1, true>(u, g, dx, w, E, stream);
-        case 54: return try_pencil<N, 1, 2, false, 3, 2, 0, true>(u, g, dx, w, E, stream);
-        case 55: return try_pencil<N, 1, 2, false, 4, 2, 0, true>(u, g, dx, w, E, stream);
+        case 47: return try_pencil<N, 1, 2, false, 1, 2, 0, true>(u, g, dx, w, E, stream, pa);
+        case 48: return try_pencil<N, 1, 2, false, 2, 2, 0, true>(u, g, dx, w, E, stream, pa);
+        case 49: return try_pencil<N, 1, 2, false, 1, 2, 0, false>(u, g, dx, w, E, stream, pa);
+        case 50: return try_pencil<N, 1, 3, false, 1, 2, 0, true>(u, g, dx, w, E, stream, pa);
+        case 51: return try_pencil<N, 1, 1, false, 3, 2, 0, true>(u, g, dx, w, E, stream, pa);
+        case 52: return try_pencil<N, 1, 3, false, 1, 2, 1, true>(u, g, dx, w, E, stream, pa);
+        case 53: return try_pencil<N, 1, 2, false, 1, 2, 1, true>(u, g, dx, w, E, stream, pa);
+        case 54: return try_pencil<N, 1, 2, false, 3, 2, 0, true>(u, g, dx, w, E, stream, pa);
+        case 55: return try_pencil<N, 1, 2, false, 4, 2, 0, true>(u, g, dx, w, E, stream, pa);
         // half-pencil kernel (two threads per k-pencil)
         case 56: return launch_half<N, 1, 2, true>(u, g, dx, w, E, stream);
         case 57: return launch_half<N, 2, 2, true>(u, g, dx, w, E, stream);
@@ -523,28 +574,35 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
         case 60: return launch_half<N, 1, 4, true>(u, g, dx, w, E, stream);
         // large n, the B stack aliasing U (dead after S1/S2: one stack less per
         // element, one extra barrier): register ring + own element L2-prefetched
-        case 61: return try_pencil<N, 1, 2, false, 2, 2, 0, true, 0, true>(u, g, dx, w, E, stream);
-        case 62: return try_pencil<N, 1, 2, false, 3, 2, 0, true, 0, true>(u, g, dx, w, E, stream);
+        case 61: return try_pencil<N, 1, 2, false, 2, 2, 0, true, 0, true>(u, g, dx, w, E, stream, pa);
+        case 62: return try_pencil<N, 1, 2, false, 3, 2, 0, true, 0, true>(u, g, dx, w, E, stream, pa);
         // TMA-staged metric + w written back by one bulk store per element
-        case 63: return try_pencil<N, 1, 3, false, 1, false, 1, true, 0, false, true>(u, g, dx, w, E, stream);
-        case 64: return try_pencil<N, 1, 2, false, 1, false, 1, true, 0, false, true>(u, g, dx, w, E, stream);
+        case 63: return try_pencil<N, 1, 3, false, 1, false, 1, true, 0, false, true>(u, g, dx, w, E, stream, pa);
+        case 64: return try_pencil<N, 1, 2, false, 1, false, 1, true, 0, false, true>(u, g, dx, w, E, stream, pa);
+        // split element: the two k-halves on a 2-CTA cluster (ax_split.cuh)
+        case 65: return launch_split<N, 6, 1, true, true>(u, g, dx, w, E, stream, pdl);
+        case 66: return launch_split<N, 5, 1, true, false>(u, g, dx, w, E, stream, pdl);
+        case 67: return launch_split<N, 4, 0, true, true>(u, g, dx, w, E, stream, pdl);
+        case 68: return launch_split<N, 6, 0, true, true>(u, g, dx, w, E, stream, pdl);
+        case 69: return launch_split<N, 3, 0, true, true>(u, g, dx, w, E, stream, pdl);
+        case 70: return launch_split<N, 8, 0, true, true>(u, g, dx, w, E, stream, pdl);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
-        case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream);
-        case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream);
-        case 4: return try_pencil<N, (S + 1) / 2, 2, false, 2>(u, g, dx, w, E, stream);
-        case 5: return try_pencil<N, (S + 1) / 2, 2, false, 3>(u, g, dx, w, E, stream);
-        case 6: return try_pencil<N, (S + 2) / 3, 3, false>(u, g, dx, w, E, stream);
-        case 7: return try_pencil<N, (S + 2) / 3, 3, false, 2>(u, g, dx, w, E, stream);
-        case 8: return try_pencil<N, (S + 2) / 3, 3, false, 3>(u, g, dx, w, E, stream);
-        case 9: return try_pencil<N, 1, 6, false, 2>(u, g, dx, w, E, stream);
-        case 10: return try_pencil<N, (S + 2) / 3, 3, false, 1, true>(u, g, dx, w, E, stream);
-        case 11: return try_pencil<N, S + 1, 1, false, 2>(u, g, dx, w, E, stream);
-        case 12: return try_pencil<N, 1, 7, false, 1>(u, g, dx, w, E, stream);
-        case 13: return try_pencil<N, 1, 7, false, 2>(u, g, dx, w, E, stream);
-        case 14: return try_pencil<N, 1, 7, false, 3>(u, g, dx, w, E, stream);
-        case 15: return try_pencil<N, 1, 5, false, 3>(u, g, dx, w, E, stream);
-        case 16: return try_pencil<N, 1, 6, false, 3>(u, g, dx, w, E, stream);
-        case 17: return try_pencil<N, (S + 1) / 2, 2, false, 4>(u, g, dx, w, E, stream);
+        case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream, pa);
+        case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream, pa);
+        case 4: return try_pencil<N, (S + 1) / 2, 2, false, 2>(u, g, dx, w, E, stream, pa);
+        case 5: return try_pencil<N, (S + 1) / 2, 2, false, 3>(u, g, dx, w, E, stream, pa);
+        case 6: return try_pencil<N, (S + 2) / 3, 3, false>(u, g, dx, w, E, stream, pa);
+        case 7: return try_pencil<N, (S + 2) / 3, 3, false, 2>(u, g, dx, w, E, stream, pa);
+        case 8: return try_pencil<N, (S + 2) / 3, 3, false, 3>(u, g, dx, w, E, stream, pa);
+        case 9: return try_pencil<N, 1, 6, false, 2>(u, g, dx, w, E, stream, pa);
+        case 10: return try_pencil<N, (S + 2) / 3, 3, false, 1, true>(u, g, dx, w, E, stream, pa);
+        case 11: return try_pencil<N, S + 1, 1, false, 2>(u, g, dx, w, E, stream, pa);
+        case 12: return try_pencil<N, 1, 7, false, 1>(u, g, dx, w, E, stream, pa);
+        case 13: return try_pencil<N, 1, 7, false, 2>(u, g, dx, w, E, stream, pa);
+        case 14: return try_pencil<N, 1, 7, false, 3>(u, g, dx, w, E, stream, pa);
+        case 15: return try_pencil<N, 1, 5, false, 3>(u, g, dx, w, E, stream, pa);
+        case 16: return try_pencil<N, 1, 6, false, 3>(u, g, dx, w, E, stream, pa);
+        case 17: return try_pencil<N, (S + 1) / 2, 2, false, 4>(u, g, dx, w, E, stream, pa);
         default:
             set_error("sem_ax: unknown variant %d", variant);
             return SEM_E_INVALID;

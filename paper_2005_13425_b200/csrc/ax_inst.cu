@@ -11,9 +11,9 @@ namespace sem {
 
 #define SEM_AX_DEFINE(NV)                                                                    \
     int ax_entry_##NV(const double* u, const double* g, const double* dx, double* w,          \
-                      int64_t E, int variant, cudaStream_t s)                                 \
+                      int64_t E, int variant, int pdl, cudaStream_t s)                        \
     {                                                                                         \
-        return ax_n<NV>(u, g, dx, w, E, variant, s);                                          \
+        return ax_n<NV>(u, g, dx, w, E, variant, pdl, s);                                     \
     }                                                                                         \
     int ax_cg_entry_##NV(const double* g, const double* dx, double* w, int64_t E,             \
                          CgpArgs a, int mode, cudaStream_t s)                                 \

@@ -344,6 +344,25 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         }
     } else if constexpr (CGM != 0) {
         griddep_wait();
+    } else {
+        // plain Ax launched as a programmatic dependent: wait for the
+        // predecessor to complete, then let our own dependent launch (its
+        // CTAs take residency while this grid drains and wait the same way)
+        if (cgp.pdl) {
+            // before waiting: pull this CTA's u and g blocks into L2.  A bulk
+            // L2 prefetch is only a hint (L2 is the coherence point; nothing
+            // is read into the SM before the wait), so it is safe even if the
+            // predecessor is still writing them -- and it overlaps this
+            // grid's DRAM ramp with the predecessor's drain (pdl == 2)
+            if (cgp.pdl >= 2 && tid == 0) {
+                const int64_t e0 = batch * SLOTS;
+                const int64_t e1 = (e0 + SLOTS < num_elements) ? e0 + SLOTS : num_elements;
+                prefetch_l2_bulk(u, e0 * NNN * 8, e1 * NNN * 8, num_elements * NNN * 8);
+                prefetch_l2_bulk(g, e0 * 6 * NNN * 8, e1 * 6 * NNN * 8, num_elements * 6 * NNN * 8);
+            }
+            griddep_wait();
+            griddep_launch();
+        }
     }
     // a CTA must not retire with bulk copies into its shared memory in flight
     auto drain = [&]() {

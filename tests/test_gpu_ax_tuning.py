@@ -1,0 +1,141 @@
+"""GPU parity of every Ax tiling at the sizes where its tuning engages.
+
+* The tuned default of every n = 2..16 at E = 4096 (BASELINE config 3: the
+  p-sweep), where the wave-ahead L2 prefetch of n = 8 / 11 (pf >= 0) and the
+  pre-wait L2 prefetch of short launches are active -- at E = 37 (the
+  ragged-tail test in test_gpu_parity.py) neither is.
+* The split-element (2-CTA cluster) variants and the other alternative
+  tilings the dispatch can be pointed at.
+* Programmatic dependent launch: back-to-back applies where each consumes or
+  overwrites the previous one's buffers, eager and CUDA-graph captured, equal
+  bit-for-bit to the same applies with a device synchronisation in between.
+
+Bar: max-norm relative difference <= 1e-12 vs the C oracle
+(sembench/verify.py:37-42).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2005_13425_b200 as sb
+from paper_2005_13425_b200._lib import load
+from paper_2005_13425_b200.kernels import apply_ax_into
+
+pytestmark = pytest.mark.gpu
+
+AX_TOL = 1e-12
+
+
+def _inputs(E, n, su, sg):
+    u = sb.random_field(E, n, su, device="cuda")
+    g = sb.random_field(6 * E, n, sg, device="cuda").reshape(E, 6, n, n, n)
+    return u, g
+
+
+def _check(u, g, w, b, idx=None):
+    if idx is None:
+        ref = O.ax_layered(u.cpu().numpy(), g.cpu().numpy(), b.diff, b.diff_t)
+        got = w.cpu().numpy()
+    else:
+        ref = O.ax_layered(u[idx].cpu().numpy(), g[idx].cpu().numpy(), b.diff, b.diff_t)
+        got = w[idx].cpu().numpy()
+    return O.rel_diff(got, ref)
+
+
+@pytest.mark.parametrize("n", list(range(2, 17)))
+def test_ax_psweep_e4096_default(cuda, n):
+    E = 4096
+    u, g = _inputs(E, n, 300 + n, 400 + n)
+    b = sb.build_basis(n)
+    before = load().sem_fallback_count()
+    w = sb.apply_ax(u, sb.GeomFactors(values=g), b)
+    torch.cuda.synchronize()
+    assert load().sem_fallback_count() == before, "tuned default fell back"
+    assert _check(u, g, w, b) <= AX_TOL
+
+
+# split-element cluster kernels (65..70) and alternative pencil tilings
+SPLIT = [65, 66, 67, 68, 69, 70]
+
+
+@pytest.mark.parametrize("n", [3, 4, 8, 10, 11, 14, 16])
+@pytest.mark.parametrize("E", [1, 37, 4096])
+def test_ax_split_variants(cuda, n, E):
+    u, g = _inputs(E, n, 500 + n, 600 + n)
+    b = sb.build_basis(n)
+    idx = sorted({0, E // 3, E // 2, E - 1}) if E > 64 else None
+    for v in SPLIT:
+        w = torch.full_like(u, float("nan"))
+        apply_ax_into(u, g, b, w, v)
+        torch.cuda.synchronize()
+        assert not torch.isnan(w).any(), f"variant {v}: unwritten output"
+        assert _check(u, g, w, b, idx) <= AX_TOL, f"variant {v}"
+
+
+@pytest.mark.parametrize("n", [8, 10, 11])
+def test_ax_alternative_tilings_e4096(cuda, n):
+    """The wave-ahead L2-prefetch tilings (40, 41, 52, 53) and the TMA
+    variants (34, 38, 63, 64) at a size where the prefetch distance is >= 0."""
+    E = 4096
+    u, g = _inputs(E, n, 700 + n, 800 + n)
+    b = sb.build_basis(n)
+    idx = list(range(0, E, 97)) + [E - 1]
+    ref = O.ax_layered(u[idx].cpu().numpy(), g[idx].cpu().numpy(), b.diff, b.diff_t)
+    for v in (34, 38, 40, 41, 52, 53, 63, 64):
+        w = torch.empty_like(u)
+        apply_ax_into(u, g, b, w, v)
+        torch.cuda.synchronize()
+        assert O.rel_diff(w[idx].cpu().numpy(), ref) <= AX_TOL, f"variant {v}"
+
+
+def _chain(bufs, g, b, v):
+    """w1 = A u; w2 = A w1; u <- A w2 (overwrites the first input); w1 <- A u."""
+    u, w1, w2 = bufs
+    apply_ax_into(u, g, b, w1, v)
+    apply_ax_into(w1, g, b, w2, v)
+    apply_ax_into(w2, g, b, u, v)
+    apply_ax_into(u, g, b, w1, v)
+
+
+@pytest.mark.parametrize("E,v", [(1024, 0), (4096, 0), (1024, 65), (512, 34)])
+def test_ax_pdl_dependent_chain(cuda, E, v):
+    n = 10
+    b = sb.build_basis(n)
+    u0, g = _inputs(E, n, 11, 12)
+    g = g * 0.05  # keep four repeated applies in range
+    # reference: a device synchronisation between consecutive applies
+    ref = [u0.clone(), torch.empty_like(u0), torch.empty_like(u0)]
+    u, w1, w2 = ref
+    for src, dst in ((u, w1), (w1, w2), (w2, u), (u, w1)):
+        apply_ax_into(src, g, b, dst, v)
+        torch.cuda.synchronize()
+    # eager back-to-back
+    eager = [u0.clone(), torch.empty_like(u0), torch.empty_like(u0)]
+    torch.cuda.synchronize()
+    _chain(eager, g, b, v)
+    torch.cuda.synchronize()
+    for a, r in zip(eager, ref):
+        assert torch.equal(a, r)
+    # captured in a CUDA graph (programmatic edges between the nodes)
+    graph_bufs = [u0.clone(), torch.empty_like(u0), torch.empty_like(u0)]
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side), torch.cuda.graph(graph, stream=side):
+        _chain(graph_bufs, g, b, v)
+    torch.cuda.current_stream().wait_stream(side)
+    graph_bufs[0].copy_(u0)
+    graph.replay()
+    torch.cuda.synchronize()
+    for a, r in zip(graph_bufs, ref):
+        assert torch.equal(a, r)
+    # and one apply against the oracle, so the chain is not trivially equal
+    w = torch.empty_like(u0)
+    apply_ax_into(u0, g, b, w, v)
+    torch.cuda.synchronize()
+    idx = [0, E // 2, E - 1]
+    ref1 = O.ax_layered(u0[idx].cpu().numpy(), g[idx].cpu().numpy(), b.diff, b.diff_t)
+    assert O.rel_diff(w[idx].cpu().numpy(), ref1) <= AX_TOL
+    assert float(np.abs(ref[1].cpu().numpy()).max()) > 0
