@@ -134,7 +134,7 @@ int mask_slab(const double* f, double* out, const Box& b, int n, cudaStream_t s)
 }
 
 int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
-                int n, int variant, cudaStream_t stream);
+                int n, int variant, cudaStream_t stream, int pdl = -1);
 
 }  // namespace sem
 

@@ -51,9 +51,9 @@ static int ax_pdl()
 }
 
 int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
-                int n, int variant, cudaStream_t stream)
+                int n, int variant, cudaStream_t stream, int pdl)
 {
-    const int pdl = ax_pdl();
+    if (pdl < 0) pdl = ax_pdl();
     switch (n) {
 #define SEM_AX_CASE(NV) \
     case NV: return ax_entry_##NV(u, g, dx, w, E, variant, pdl, stream);
@@ -80,7 +80,7 @@ extern "C" int sem_ax_variant(const double* u, const double* g, const double* dx
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (int rc = sem::bind_stream_device(s)) return rc;
-    return sem::ax_dispatch(u, g, dx, w, num_elements, n, variant, s);
+    return sem::ax_dispatch(u, g, dx, w, num_elements, n, variant, s, -1);
 }
 
 extern "C" int sem_ax(const double* u, const double* g, const double* dx,

@@ -170,12 +170,16 @@ __device__ __forceinline__ void pencil_gemv(const DParamP<N>& D, int st, const d
 __device__ __forceinline__ void prefetch_l2_bulk(const void* base, int64_t lo, int64_t hi,
                                                  int64_t limit)
 {
-    lo &= ~int64_t(15);
-    hi = (hi + 15) & ~int64_t(15);
-    if (hi > (limit & ~int64_t(15))) hi = limit & ~int64_t(15);
-    if (hi <= lo) return;
-    const char* p = static_cast<const char*>(base) + lo;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)(hi - lo))
+    // 16-byte granularity on the ABSOLUTE address (a field may start at any
+    // 8-byte boundary, e.g. a staged host buffer), kept inside [base, base+limit)
+    const uint64_t b = reinterpret_cast<uint64_t>(base);
+    uint64_t a0 = (b + (uint64_t)lo) & ~uint64_t(15);
+    uint64_t a1 = (b + (uint64_t)(hi < limit ? hi : limit) + 15) & ~uint64_t(15);
+    const uint64_t first = (b + 15) & ~uint64_t(15), last = (b + (uint64_t)limit) & ~uint64_t(15);
+    if (a0 < first) a0 = first;
+    if (a1 > last) a1 = last;
+    if (a1 <= a0) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0))
                  : "memory");
 }
 
@@ -315,7 +319,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     // otherwise one batch per CTA (D constants are not loop-invariant, so
     // the compiler keeps them in uniform registers only around their use).
 
-    double beta = 0.0, alpha_prev = 0.0;
+    double beta = 0.0, alpha_prev = 0.0, pap_s = 1.0;
     bool xpend = false;
     // GMODE 4: every bulk copy of the CTA (p, r, x, g) is issued before the
     // CG scalars are read, so the state round trip overlaps the transfers;
@@ -390,6 +394,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             return;
         }
         beta = (it == 1) ? 0.0 : rtz / st->rtz_old;
+        pap_s = ldexp(1.0, pap_scale_exp(rtz));  // exact power of two (fin_pap)
         xpend = st->x_pending != 0;
         alpha_prev = st->alpha;
         if (blockIdx.x == 0 && tid == 0) st->beta = beta;
@@ -647,7 +652,8 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             for (int k = 0; k < N; ++k) {
                 const double v = (A[k * LSA + kp] + B[k * LSB + kp]) + Wt[k];
                 __stcs(we + k * NN, v);
-                if constexpr (CGM != 0) pap_acc = fma(U[k * LSU + kp], v, pap_acc);  // U = p_new
+                if constexpr (CGM != 0)  // U = p_new; scaled by pap_s^2 (fin_pap)
+                    pap_acc = fma(pap_s * U[k * LSU + kp], pap_s * v, pap_acc);
             }
         }
         // (no barrier needed: the next S3 writes only U, last read before the
@@ -687,12 +693,13 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
                 return;
             }
             st->x_pending = 0;  // every CTA applied it above
-            st->pap = pap;
+            const int k = pap_scale_exp(st->rtz);  // pap is scaled by 2^(2k)
+            st->pap = ldexp(pap, -2 * k);
             if (pap <= 0.0) {   // cg.py:164-169 breakdown
                 st->stop = 2;
                 st->breakdown_it = st->it + 1;
             } else {
-                st->alpha = st->rtz / pap;
+                st->alpha = ldexp(st->rtz, 2 * k) / pap;
             }
         }
     }

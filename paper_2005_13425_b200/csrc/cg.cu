@@ -41,7 +41,7 @@
 namespace sem {
 
 int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
-                int n, int variant, cudaStream_t stream);
+                int n, int variant, cudaStream_t stream, int pdl = -1);
 int ax_cg_dispatch(const double* g, const double* dx, double* w, int64_t E, int n, CgpArgs a,
                    int mode, cudaStream_t stream);
 
@@ -139,15 +139,19 @@ __device__ __forceinline__ void fin_init(sem_cg_state* st, double rtz)
     st->x_pending = 0;
 }
 
-__device__ __forceinline__ void fin_pap(sem_cg_state* st, double pap)
+// pap_s: <p, A p> as the fused kernels accumulate it, scaled by
+// 2^(2k), k = pap_scale_exp(rtz) (sem_common.cuh): alpha = (rtz 2^(2k)) / pap_s
+// is the unscaled rtz / pap bit for bit in the normal range
+__device__ __forceinline__ void fin_pap(sem_cg_state* st, double pap_s)
 {
-    st->pap = pap;
+    const int k = pap_scale_exp(st->rtz);
+    st->pap = ldexp(pap_s, -2 * k);  // reported value (may underflow)
     st->x_pending = 0;  // the Ax prologues of this iteration applied it
-    if (pap <= 0.0) {  // cg.py:164-169 breakdown
+    if (pap_s <= 0.0) {  // cg.py:164-169 breakdown
         st->stop = 2;
         st->breakdown_it = st->it + 1;
     } else {
-        st->alpha = st->rtz / pap;
+        st->alpha = ldexp(st->rtz, 2 * k) / pap_s;
     }
 }
 
@@ -227,26 +231,37 @@ static unsigned row_grid(int64_t E)
     return (unsigned)(blocks < kReduceBlocks ? (blocks > 0 ? blocks : 1) : kReduceBlocks);
 }
 
-// update2 grid: ONE full wave of the row kernel -- SEM_UPD_MINB (6) blocks
-// of 128 threads per SM x 148 SMs -- each thread walking its rows
-// grid-stride (tools/upd_minb2.sh: one wave beat 1.3-2 waves by 10-25%).
-// 3 x 256 threads measured ~1% faster per CG iteration (tools/
-// row_threads.sh, profiles/r01_cg_row_threads.txt) but its reduction tree
-// sent the reference's own manufactured-solution property (verify.py:
+// update2 grid: ONE full wave of the row kernel -- 768 threads per SM
+// (6 blocks of 128 threads, or 3 of 256) x 148 SMs -- each thread walking its
+// rows grid-stride (tools/upd_minb2.sh: one wave beat 1.3-2 waves by 10-25%).
+// 3 x 256 threads measured ~1% faster per CG iteration than 6 x 128 (tools/
+// row_threads.sh, profiles/r01_cg_row_threads.txt); in round 1 its reduction
+// tree sent the reference's own manufactured-solution property (verify.py:
 // 457-476: 1331 iterations at tol 0, deep into FP64 underflow) into a
-// <p, A p> = 0 breakdown, so the verified tree is kept.  A constant (a
-// function of E and n only, never of the device), so the tree is fixed.
+// <p, A p> = 0 breakdown, so 128 stayed.  With <p, A p> accumulated at an
+// exact power-of-two scale (fin_pap) both trees pass (tests/
+// test_gpu_parity.py pins both), so 256 is the default; SEM_CG_ROW_THREADS
+// = 128 (read per solve) selects the other.  The grid is a function of E and
+// n only, never of the device, so the tree is fixed.
 constexpr int kUpdBlocks = SEM_UPD_MINB * 148;
 static_assert(kUpdBlocks <= kReduceBlocksMax, "update grid exceeds the partial slots");
 
-template <int N>
+template <int N, int RT = kRowThreads>
 static unsigned upd_grid(int64_t E)
 {
     static const int cap = getenv("SEM_CG_UPD_BLOCKS") ? atoi(getenv("SEM_CG_UPD_BLOCKS")) : 0;
     const int64_t rows = E * N * N;
-    int64_t blocks = std::min<int64_t>(kUpdBlocks, (rows + kRowThreads - 1) / kRowThreads);
+    constexpr int64_t kBlocks = (int64_t)kUpdBlocks * kRowThreads / RT;
+    int64_t blocks = std::min<int64_t>(kBlocks, (rows + RT - 1) / RT);
     if (cap > 0 && cap <= kReduceBlocksMax) blocks = std::min<int64_t>(rows, cap);
     return (unsigned)(blocks > 0 ? blocks : 1);
+}
+
+// threads per update block (SEM_CG_ROW_THREADS: 256 default, or 128)
+static int upd_row_threads()
+{
+    const char* env = getenv("SEM_CG_ROW_THREADS");
+    return (env && atoi(env) == kRowThreads) ? kRowThreads : 256;
 }
 
 template <int N>
@@ -265,8 +280,8 @@ static int cg_init_n(const double* f, double* x, double* r, double* p, sem_cg_st
 // gather of rows.cuh (faces shared with another rank from the halo planes),
 // and <r, r>_c -> history, tolerance flag, beta's numerator (DIST: this
 // rank's partial -> state->local_sum, combined by sem_cg_finish).
-template <int N, bool DIST>
-__global__ void __launch_bounds__(kRowThreads, SEM_UPD_MINB)
+template <int N, bool DIST, int RT = kRowThreads>
+__global__ void __launch_bounds__(RT, SEM_UPD_MINB * kRowThreads / RT)
 cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, BoxFlat bf,
                   sem_cg_state* st, double* history, ReduceScratch* rs,
                   const double* __restrict__ bot, const double* __restrict__ top,
@@ -277,8 +292,8 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     if (st->stop) return;
     const double nalpha = -st->alpha;
     double acc = 0.0;
-    for (int64_t row = (int64_t)blockIdx.x * kRowThreads + threadIdx.x; row < E * NN;
-         row += (int64_t)gridDim.x * kRowThreads) {
+    for (int64_t row = (int64_t)blockIdx.x * RT + threadIdx.x; row < E * NN;
+         row += (int64_t)gridDim.x * RT) {
         const Box& bx = bf.b;
         const Row<N> rw = make_row<N>(row, bf);
         const int64_t base = rw.e * NNN + rw.jk * N;
@@ -295,10 +310,10 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     griddep_launch();
     const double vals[1] = {acc};
     if (deferred) {  // single GPU: cg_settle_kernel finishes <r, r>
-        reduce_publish_only<1, kRowThreads>(vals, rs);
+        reduce_publish_only<1, RT>(vals, rs);
         return;
     }
-    reduce_publish_and_finish<1, kRowThreads>(vals, rs, [&](const double (&t)[1]) {
+    reduce_publish_and_finish<1, RT>(vals, rs, [&](const double (&t)[1]) {
         if (DIST) st->local_sum = t[0];
         else fin_rr(st, t[0], history);
     });
@@ -381,6 +396,7 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
     // its predecessor drains and waits on it in-kernel (griddep_wait)
     // (SEM_CG_PDL=1: every launch; 2: the settle and update launches only)
     const bool pdl = cg_pdl() != 0 && marks == nullptr;
+    const bool rt256 = upd_row_threads() == 256;
     unsigned ax_grid = 0;
     const CgpArgs a{p, r, st, history, x, w2, &rs->counter, 0, defer_ax ? 1 : 0, &ax_grid,
                     (pdl && cg_pdl() == 1) ? 1 : 0};
@@ -396,10 +412,15 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
         }
         if (cudaError_t e = mark(3 * it + 1)) return fail_cuda(e, "sem_cg_run: event");
         if (defer) {
-            const unsigned ug = upd_grid<N>(E);
-            if (int rc = chk(launch_k(cg_update2_kernel<N, false>, dim3(ug), dim3(kRowThreads), 0, s,
-                                      pdl, (const double*)w, r, E, make_box_flat(bx), st, history,
-                                      rs, (const double*)nullptr, (const double*)nullptr, true),
+            const unsigned ug = rt256 ? upd_grid<N, 256>(E) : upd_grid<N>(E);
+            if (int rc = chk(rt256 ? launch_k(cg_update2_kernel<N, false, 256>, dim3(ug), dim3(256), 0, s,
+                                              pdl, (const double*)w, r, E, make_box_flat(bx), st,
+                                              history, rs, (const double*)nullptr,
+                                              (const double*)nullptr, true)
+                                   : launch_k(cg_update2_kernel<N, false>, dim3(ug), dim3(kRowThreads), 0,
+                                              s, pdl, (const double*)w, r, E, make_box_flat(bx), st,
+                                              history, rs, (const double*)nullptr,
+                                              (const double*)nullptr, true),
                              "cg update kernel"))
                 return rc;
             if (int rc = chk(launch_k(cg_settle_kernel<2>, dim3(1), dim3(kSettleThreads), 0, s, pdl,
@@ -407,10 +428,14 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
                              "cg settle (rr)"))
                 return rc;
         } else {
-            if (int rc = chk(launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
-                                      dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E,
-                                      make_box_flat(bx), st, history, rs, (const double*)nullptr,
-                                      (const double*)nullptr, false),
+            if (int rc = chk(rt256 ? launch_k(cg_update2_kernel<N, false, 256>, dim3(upd_grid<N, 256>(E)),
+                                              dim3(256), 0, s, pdl, (const double*)w, r, E,
+                                              make_box_flat(bx), st, history, rs,
+                                              (const double*)nullptr, (const double*)nullptr, false)
+                                   : launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
+                                              dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E,
+                                              make_box_flat(bx), st, history, rs,
+                                              (const double*)nullptr, (const double*)nullptr, false),
                              "cg update kernel"))
                 return rc;
         }

@@ -19,7 +19,7 @@
 namespace sem {
 
 int ax_dispatch(const double* u, const double* g, const double* dx, double* w, int64_t E,
-                int n, int variant, cudaStream_t stream);
+                int n, int variant, cudaStream_t stream, int pdl = -1);
 
 namespace {
 
@@ -131,7 +131,7 @@ extern "C" int sem_ax_host(const double* u_host, const double* g, const double* 
         // 0.894 vs 0.904 ms; on device memory the bulk store is 5% slower,
         // so device-resident calls keep the default)
         const int zv = (n == 10) ? 63 : 0;
-        return ax_dispatch(u_map, g, dx, w_map, num_elements, n, zv, s);
+        return ax_dispatch(u_map, g, dx, w_map, num_elements, n, zv, s, 1);  // no L2 prefetch of host memory
     }
     int64_t sizes[kMaxChunks];
     const int nchunks = chunk_schedule(num_elements, chunk_elements, sizes);

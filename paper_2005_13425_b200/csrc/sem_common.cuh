@@ -82,3 +82,17 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 // vector updates are unfused multiply-then-add (sembench/cg.py:95-104).
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+// Exact power-of-two scale for the fused <p, A p> sum: 2^k with rtz * 2^(2k)
+// in [1, 8).  The CG kernels accumulate (s p) * (s w) and divide s^2 back out
+// of rtz instead of pap, so in the normal range every product and partial
+// sum is the unscaled one times an exact power of two (alpha bit-identical),
+// while deep in FP64 underflow the scaled <p, A p> cannot flush to zero
+// before <r, r> does -- breakdown is then decided by the sign of <p, A p>,
+// not by which reduction tree underflows first.
+__device__ __forceinline__ int pap_scale_exp(double rtz)
+{
+    if (!(rtz > 0.0) || !isfinite(rtz)) return 0;
+    return -(ilogb(rtz) >> 1);
+}
+

@@ -417,8 +417,36 @@ def test_cg_counter_identity(cuda):
     assert counters.flops == 5 * (sb.flops_per_apply(dofs, 5) + 12 * dofs)
 
 
-def test_cg_manufactured_solution(cuda):
-    # verify.py:457-476 on 4^3 elements, n=4
+def test_cg_full_size_e32768_vs_oracle(cuda):
+    """BASELINE config 5's per-GPU size ("a few iterations at
+    full size"): 32 x 32 x 32 elements, n = 10 (32.8 M points), the fused
+    solver vs the C oracle's CG for 5 iterations -- residual history within
+    1e-10, solution within 1e-10."""
+    ex = ey = ez = 32
+    n, E, iters = 10, 32768, 5
+    b = sb.build_basis(n)
+    mesh = sb.build_mesh(ex, ey, ez, n, 1.0)
+    topo = sb.build_topology(mesh)
+    geom = sb.build_geom(mesh, b, device="cuda")
+    f = sb.make_rhs(E, n, topo, sb.mix64(1, E))
+    res = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(iters, 0.0))
+    del geom
+    T = O.BoxTopology(ex, ey, ez, n)
+    gh = O.box_geom(ex, ey, ez, b.weights, 1.0)
+    x, hist, it = O.cg(f, lambda p: O.apply_global(p, gh, b.diff, b.diff_t, T), T, iters)
+    assert it == iters == res.iterations_run
+    assert _rel_hist(res.residual_history, hist) <= CG_TOL
+    assert O.rel_diff(_np(res.solution), x) <= CG_TOL
+
+
+@pytest.mark.parametrize("row_threads", ["128", "256"])
+def test_cg_manufactured_solution(cuda, monkeypatch, row_threads):
+    # verify.py:457-476 on 4^3 elements, n=4: 1331 iterations at tol 0, far
+    # past convergence into FP64 underflow.  The fused <p, A p> is summed at
+    # an exact power-of-two scale (fin_pap), so whether the solve ends on
+    # <r, r> == 0 or on a breakdown no longer depends on the update kernel's
+    # reduction tree: both block sizes must pass (round 1: 256 broke down).
+    monkeypatch.setenv("SEM_CG_ROW_THREADS", row_threads)
     b = sb.build_basis(4)
     mesh = sb.build_mesh(4, 4, 4, 4, 1.0)
     topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b)
