@@ -252,6 +252,16 @@ int sem_cg_update_slab(const double *w, double *r, const double *bottom_totals,
                        sem_stream_t stream);
 int sem_cg_finish(sem_cg_state *state, const double *gathered, int32_t nranks, int32_t phase,
                   double *history, sem_stream_t stream);
+/* sem_cg_finish(phase 1) folded into sem_cg_update_slab: every CTA combines
+ * the ranks' <p,Ap> partials `gathered_pap[0..nranks)` in rank order and
+ * derives alpha itself (breakdown -> stop = 2, r untouched), then the update.
+ * One launch per iteration fewer (replaces sem_cg_finish(state, ., ., 1, .)
+ * + sem_cg_update_slab; the sembench recurrence cg.py:163-172). */
+int sem_cg_update_slab_alpha(const double *w, double *r, const double *bottom_totals,
+                             const double *top_totals, sem_cg_state *state,
+                             const double *gathered_pap, int32_t nranks, int32_t ex, int32_t ey,
+                             int32_t ez, int32_t n, int32_t gz0, int32_t ez_global,
+                             void *scratch, sem_stream_t stream);
 
 /* ------------------------------------------------------ input builders -- */
 int sem_random_field(double *out, int64_t count, uint64_t seed, sem_stream_t stream);

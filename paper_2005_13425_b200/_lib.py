@@ -91,6 +91,8 @@ SIGNATURES = {
     "sem_cg_settle_slab": (ctypes.c_int, [_vp, _i64, _vp, _i32, _vp]),
     "sem_cg_update_slab": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                                           _i32, _vp, _vp]),
+    "sem_cg_update_slab_alpha": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,
+                                                _i32, _i32, _i32, _i32, _vp, _vp]),
     "sem_cg_finish": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
     "sem_random_field": (ctypes.c_int, [_vp, _i64, ctypes.c_uint64, _vp]),
     "sem_box_geom": (ctypes.c_int, [_vp, _i64, _i32, _dp, _f64, _vp]),

@@ -285,12 +285,26 @@ __global__ void __launch_bounds__(RT, SEM_UPD_MINB * kRowThreads / RT)
 cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E, BoxFlat bf,
                   sem_cg_state* st, double* history, ReduceScratch* rs,
                   const double* __restrict__ bot, const double* __restrict__ top,
-                  bool deferred = false)
+                  bool deferred = false, const double* __restrict__ gathered = nullptr,
+                  int nranks = 0)
 {
     constexpr int NN = N * N, NNN = N * N * N;
     griddep_wait();
     if (st->stop) return;
-    const double nalpha = -st->alpha;
+    double alpha;
+    if (DIST && gathered != nullptr) {
+        // multi-GPU phase-1 finish folded in: every CTA combines the ranks'
+        // <p, A p> partials in rank order (the same sum cg_finish_kernel
+        // forms) and derives alpha itself; block 0 records the state
+        double pap_s = 0.0;
+        for (int q = 0; q < nranks; ++q) pap_s += __ldg(gathered + q);
+        if (blockIdx.x == 0 && threadIdx.x == 0) fin_pap(st, pap_s);
+        if (pap_s <= 0.0) return;  // breakdown (block 0 set stop = 2)
+        alpha = ldexp(st->rtz, 2 * pap_scale_exp(st->rtz)) / pap_s;
+    } else {
+        alpha = st->alpha;
+    }
+    const double nalpha = -alpha;
     double acc = 0.0;
     for (int64_t row = (int64_t)blockIdx.x * RT + threadIdx.x; row < E * NN;
          row += (int64_t)gridDim.x * RT) {
@@ -322,10 +336,11 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
 template <int N, bool DIST>
 static void launch_update(const double* w, double* r, int64_t E, const Box& bx, sem_cg_state* st,
                           double* history, ReduceScratch* rs, const double* bot,
-                          const double* top, cudaStream_t s)
+                          const double* top, cudaStream_t s, const double* gathered = nullptr,
+                          int nranks = 0)
 {
-    cg_update2_kernel<N, DIST><<<upd_grid<N>(E), kRowThreads, 0, s>>>(w, r, E, make_box_flat(bx),
-                                                                     st, history, rs, bot, top);
+    cg_update2_kernel<N, DIST><<<upd_grid<N>(E), kRowThreads, 0, s>>>(
+        w, r, E, make_box_flat(bx), st, history, rs, bot, top, false, gathered, nranks);
 }
 
 // Finish a deferred reduction of the single-GPU iteration: the fixed-order
@@ -416,11 +431,11 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
             if (int rc = chk(rt256 ? launch_k(cg_update2_kernel<N, false, 256>, dim3(ug), dim3(256), 0, s,
                                               pdl, (const double*)w, r, E, make_box_flat(bx), st,
                                               history, rs, (const double*)nullptr,
-                                              (const double*)nullptr, true)
+                                              (const double*)nullptr, true, (const double*)nullptr, 0)
                                    : launch_k(cg_update2_kernel<N, false>, dim3(ug), dim3(kRowThreads), 0,
                                               s, pdl, (const double*)w, r, E, make_box_flat(bx), st,
                                               history, rs, (const double*)nullptr,
-                                              (const double*)nullptr, true),
+                                              (const double*)nullptr, true, (const double*)nullptr, 0),
                              "cg update kernel"))
                 return rc;
             if (int rc = chk(launch_k(cg_settle_kernel<2>, dim3(1), dim3(kSettleThreads), 0, s, pdl,
@@ -431,11 +446,11 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
             if (int rc = chk(rt256 ? launch_k(cg_update2_kernel<N, false, 256>, dim3(upd_grid<N, 256>(E)),
                                               dim3(256), 0, s, pdl, (const double*)w, r, E,
                                               make_box_flat(bx), st, history, rs,
-                                              (const double*)nullptr, (const double*)nullptr, false)
+                                              (const double*)nullptr, (const double*)nullptr, false, (const double*)nullptr, 0)
                                    : launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
                                               dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E,
                                               make_box_flat(bx), st, history, rs,
-                                              (const double*)nullptr, (const double*)nullptr, false),
+                                              (const double*)nullptr, (const double*)nullptr, false, (const double*)nullptr, 0),
                              "cg update kernel"))
                 return rc;
         }
@@ -748,6 +763,30 @@ extern "C" int sem_cg_update_slab(const double* w, double* r, const double* bott
     SEM_SWITCH_N(n, {
         launch_update<NV, true>(w, r, E, bx, state, nullptr, rs, bottom_totals, top_totals, s);
         SEM_CHECK_LAUNCH("sem_cg_update_slab launch");
+        return 0;
+    });
+}
+
+extern "C" int sem_cg_update_slab_alpha(const double* w, double* r, const double* bottom_totals,
+                                        const double* top_totals, sem_cg_state* state,
+                                        const double* gathered_pap, int32_t nranks, int32_t ex,
+                                        int32_t ey, int32_t ez, int32_t n, int32_t gz0,
+                                        int32_t ez_global, void* scratch, sem_stream_t stream)
+{
+    if (int rc = check_slab(ex, ey, ez, n, gz0, ez_global, "sem_cg_update_slab_alpha")) return rc;
+    if (!w || !r || !state || !scratch || w == r || !gathered_pap || nranks < 1) {
+        set_error("sem_cg_update_slab_alpha: bad arguments");
+        return SEM_E_INVALID;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (int rc = bind_stream_device(s)) return rc;
+    const Box bx = slab_box(ex, ey, ez, gz0, ez_global);
+    const int64_t E = (int64_t)ex * ey * ez;
+    auto* rs = static_cast<ReduceScratch*>(scratch);
+    SEM_SWITCH_N(n, {
+        launch_update<NV, true>(w, r, E, bx, state, nullptr, rs, bottom_totals, top_totals, s,
+                                gathered_pap, nranks);
+        SEM_CHECK_LAUNCH("sem_cg_update_slab_alpha launch");
         return 0;
     });
 }

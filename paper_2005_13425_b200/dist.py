@@ -16,14 +16,23 @@ solver's two kernels per rank (csrc/cg.cu):
     halo, step 1: top-face partial sums  -> rank r+1               (plane_top)
     halo, step 2: continue the prefix with own bottom-face copies
                   -> interface totals    -> rank r-1               (plane_bottom)
-    all_gather of the <p, A p> partials -> alpha                    (finish 1)
+    all_gather of the <p, A p> partials; every update CTA combines them
+         in rank order -> alpha (finish 1 folded into the update launch)
     r -= alpha mask(dssum(w)) with the faces taken from the totals,
          local <r, r>_c partial -> all_gather                (update, finish 2)
 
 and after the loop the owed x += alpha p (sem_cg_finalize).  <p, A p> is the
 sum over elements of p.(A_local p), each element owned by exactly one rank,
 so the rank partials need no halo (p is continuous and masked; see
-ax_pencil.cuh).
+ax_pencil.cuh).  The second exchange overlaps the settle of <p, A p> and
+its gather.
+
+With one rank there is no halo and no gather (the slab is the box, a rank's
+partial is the total), so the iteration is one Ax launch, one settle, the
+update and finish 2.  Over NCCL the iteration is captured once in a CUDA
+graph and replayed (the launches are parameter-stable: scalars live in the
+device state), so the driver loop is not host-bound at small slabs; early
+exits are device-side (stop flag) and polled without blocking.
 
 The two-step halo reproduces the reference's bincount order bit-for-bit:
 every copy on rank r-1's side of an interface has a lower element id than
@@ -41,6 +50,7 @@ product implementation of ``SlabOps`` is ``CudaSlabOps`` (libsem kernels).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -50,8 +60,10 @@ import torch.distributed as dist
 from . import _device as dv
 from ._lib import check, load, sem_cg_state
 
+_STOP_OFFSET = sem_cg_state.stop.offset
+
 __all__ = ["SlabPartition", "SlabComm", "CudaSlabOps", "dist_cg_solve", "dist_dssum",
-           "halo_exchange", "DistCgResult"]
+           "dist_cg_phases", "halo_exchange", "DistCgResult"]
 
 
 @dataclass(frozen=True)
@@ -168,11 +180,33 @@ class SlabComm:
 
     def exchange_down(self, bottom_totals, top_totals) -> None:
         """Send the bottom interface totals to rank-1; receive rank+1's."""
+        self.exchange_up_wait(self.exchange_down_start(bottom_totals, top_totals))
+
+    def exchange_down_start(self, bottom_totals, top_totals):
+        """Non-blocking form of exchange_down (see exchange_up_start)."""
         p = self.part
-        self._xfer([(bottom_totals, p.lower)] if p.lower is not None else [],
-                   [(top_totals, p.upper)] if p.upper is not None else [])
+        sends = [(bottom_totals, p.lower)] if p.lower is not None else []
+        recvs = [(top_totals, p.upper)] if p.upper is not None else []
+        if self.stage:
+            self._xfer(sends, recvs)
+            return None
+        ops = [dist.P2POp(dist.isend, t, peer, self.group) for t, peer in sends]
+        ops += [dist.P2POp(dist.irecv, t, peer, self.group) for t, peer in recvs]
+        return dist.batch_isend_irecv(ops) if ops else None
+
+    @property
+    def capturable(self) -> bool:
+        """Collectives of this communicator can be captured in a CUDA graph:
+        NCCL, and (untested beyond one rank on this project's hardware) for
+        world > 1 only when SEM_DIST_GRAPH=1."""
+        if self.stage:
+            return False
+        return self.part.world == 1 or os.environ.get("SEM_DIST_GRAPH", "0") == "1"
 
     def allgather(self, local: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """All ranks' partials in rank order.  One rank: the partial itself."""
+        if self.part.world == 1:
+            return local
         if self.stage and local.is_cuda:
             tmp = torch.empty(out.shape, dtype=out.dtype)
             dist.all_gather_into_tensor(tmp, local.cpu(), group=self.group)
@@ -304,6 +338,37 @@ class CudaSlabOps:
                                           ptr(top_totals), dv.ptr(self.state), *self._slab(),
                                           dv.ptr(self.scratch), self._s())), "dist update")
 
+    def update_alpha(self, bottom_totals, top_totals, gathered: torch.Tensor) -> None:
+        """finish(1) folded into the update launch: alpha from the gathered
+        <p, A p> partials (rank order) in every CTA, then update()."""
+        ptr = lambda t: dv.ptr(t) if t is not None else ctypes.c_void_p(0)  # noqa: E731
+        key = ("update_alpha", None if bottom_totals is None else bottom_totals.data_ptr(),
+               None if top_totals is None else top_totals.data_ptr(), gathered.data_ptr(),
+               gathered.numel())
+        self._invoke(key, lambda: (
+            self.lib.sem_cg_update_slab_alpha, (dv.ptr(self.w), dv.ptr(self.r), ptr(bottom_totals),
+                                                ptr(top_totals), dv.ptr(self.state),
+                                                dv.ptr(gathered), gathered.numel(), *self._slab(),
+                                                dv.ptr(self.scratch), self._s())),
+            "dist update (alpha)")
+
+    def iteration_graph(self, enqueue):
+        """CUDA graph of one iteration (`enqueue()` launches it), captured on
+        a side stream once per ops object."""
+        if getattr(self, "_graph", None) is None:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(self.dev)
+            side.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+                enqueue()
+            torch.cuda.current_stream(self.dev).wait_stream(side)
+            self._graph = g
+        return self._graph
+
+    def stop_flag(self) -> torch.Tensor:
+        """Device int32 view of sem_cg_state.stop (early-exit polling)."""
+        return self.state[_STOP_OFFSET:_STOP_OFFSET + 4].view(torch.int32)
+
     def finalize(self) -> None:
         """The owed x += alpha p of the last iteration run."""
         check(self.lib.sem_cg_finalize(dv.ptr(self.x), dv.ptr(self.p), dv.ptr(self.state),
@@ -349,28 +414,87 @@ class DistCgResult:
     stop: int
 
 
-def dist_cg_solve(ops, comm: SlabComm, f_local, max_iterations: int, tolerance: float = 0.0
-                  ) -> DistCgResult:
-    """Distributed CG; every rank calls this with its slab (same arguments)."""
+def _ax_ranges(part: SlabPartition):
+    """(edge ranges, interior range or None): with a neighbour the interface
+    planes need only the bottom / top element layers, so they go first and
+    the interior overlaps the first exchange; without one, one launch."""
+    ez = part.ez
+    if part.lower is None and part.upper is None:
+        return [(0, ez)], None
+    edge = [(0, 1)] if ez == 1 else [(0, 1), (ez - 1, ez)]
+    return edge, ((1, ez - 1) if ez > 2 else None)
+
+
+def _iteration(ops, comm: SlabComm, gathered, phase=None) -> None:
+    """Enqueue one distributed CG iteration (every rank).  `phase(name)`, if
+    given, is called at each phase boundary (instrumentation)."""
+    mark = phase or (lambda name: None)
     part = comm.part
-    world = part.world
-    gathered = ops.scalar_buffer(world)
+    edge, interior = _ax_ranges(part)
+    mark("ax")
+    for q, (l0, l1) in enumerate(edge):
+        ops.ax_layers(l0, l1, first=(q == 0))
+    if part.lower is None and part.upper is None:
+        bot = top = None
+    else:
+        mark("halo")
+        top_p = ops.plane_top(ops.w) if part.upper is not None else None
+        handle = comm.exchange_up_start(top_p, ops.bottom_prefix if part.lower is not None
+                                        else None)
+        if interior is not None:  # overlaps the first exchange
+            ops.ax_layers(*interior, first=False)
+        comm.exchange_up_wait(handle)
+        bot = ops.plane_bottom(ops.w, ops.bottom_prefix) if part.lower is not None else None
+        top = ops.top_totals if part.upper is not None else None
+        handle = comm.exchange_down_start(bot, top)
+    mark("pap")
+    ops.settle()  # overlaps the second exchange
+    g1 = comm.allgather(ops.local_sum(), gathered)
+    if part.lower is not None or part.upper is not None:
+        comm.exchange_up_wait(handle)
+    mark("update")
+    if hasattr(ops, "update_alpha"):
+        ops.update_alpha(bot, top, g1)
+    else:
+        ops.finish(1, g1)
+        ops.update(bot, top)
+    mark("rr")
+    ops.finish(2, comm.allgather(ops.local_sum(), gathered))
+    mark("end")
+
+
+POLL_EVERY = 8
+
+
+def dist_cg_solve(ops, comm: SlabComm, f_local, max_iterations: int, tolerance: float = 0.0,
+                  graph: bool | None = None) -> DistCgResult:
+    """Distributed CG; every rank calls this with its slab (same arguments).
+    `graph` (default: comm.capturable and a CUDA ops object) captures one
+    iteration in a CUDA graph and replays it."""
+    part = comm.part
+    gathered = ops.scalar_buffer(part.world)
     ops.init(f_local, max_iterations, tolerance)
     ops.finish(0, comm.allgather(ops.local_sum(), gathered))
-    ez = part.ez
-    # the interface planes need only the bottom and top element layers: apply
-    # the operator there first and overlap the interior with the first exchange
-    edge = [(0, 1)] if ez == 1 else [(0, 1), (ez - 1, ez)]
-    for _ in range(max_iterations):
-        for q, (l0, l1) in enumerate(edge):
-            ops.ax_layers(l0, l1, first=(q == 0))
-        bot, top = halo_exchange(ops, comm, ops.w,
-                                 overlap=lambda: ops.ax_layers(1, ez - 1, first=False)
-                                 if ez > 2 else None)
-        ops.settle()
-        ops.finish(1, comm.allgather(ops.local_sum(), gathered))
-        ops.update(bot, top)
-        ops.finish(2, comm.allgather(ops.local_sum(), gathered))
+    if graph is None:
+        graph = comm.capturable and isinstance(ops, CudaSlabOps) and max_iterations > 2
+    if not graph:
+        for _ in range(max_iterations):
+            _iteration(ops, comm, gathered)
+    else:
+        dev = ops.dev
+        _iteration(ops, comm, gathered)  # iteration 1 eagerly: configures the kernels
+        g = ops.iteration_graph(lambda: _iteration(ops, comm, gathered))
+        stream = torch.cuda.current_stream(dev)
+        stop_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        stop_event = None
+        for q in range(max_iterations - 1):
+            g.replay()
+            if (q + 1) % POLL_EVERY == 0:  # every rank sees the same flag
+                if stop_event is not None and stop_event.query() and int(stop_host[0]) != 0:
+                    break
+                stop_host.copy_(ops.stop_flag(), non_blocking=True)
+                stop_event = torch.cuda.Event()
+                stop_event.record(stream)
     ops.finalize()
     x, hist, iters, stop, pap, bit = ops.result()
     if stop == 2:
@@ -378,3 +502,31 @@ def dist_cg_solve(ops, comm: SlabComm, f_local, max_iterations: int, tolerance: 
         raise CgBreakdownError(f"<p, A p>_c = {pap:.3e} at iteration {bit}; "
                                "operator is not SPD here")
     return DistCgResult(solution=x, residual_history=hist, iterations_run=iters, stop=stop)
+
+
+def dist_cg_phases(ops, comm: SlabComm, f_local, iterations: int) -> dict:
+    """Per-rank device time (ms, summed over `iterations` eager iterations)
+    of the iteration's phases -- ax (Ax launches up to the first exchange),
+    halo (planes, exchanges, overlapped interior Ax), pap (settle + gather),
+    update (alpha + r update), rr (gather + finish) -- from CUDA events on
+    the compute stream.  Measurement only (bench.py --gpus N)."""
+    part = comm.part
+    gathered = ops.scalar_buffer(part.world)
+    ops.init(f_local, iterations, 0.0)
+    ops.finish(0, comm.allgather(ops.local_sum(), gathered))
+    stream = torch.cuda.current_stream(ops.dev)
+    marks: list = []
+
+    def phase(name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        marks.append((name, ev))
+
+    for _ in range(iterations):
+        _iteration(ops, comm, gathered, phase)
+    torch.cuda.synchronize(ops.dev)
+    out: dict = {}
+    for (name, e0), (_, e1) in zip(marks, marks[1:]):
+        if name != "end":
+            out[name] = out.get(name, 0.0) + e0.elapsed_time(e1)
+    return out

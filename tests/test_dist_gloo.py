@@ -162,6 +162,11 @@ class NumpySlabOps:
         O.axpy_into(self.r, np.ascontiguousarray(w2), -a)
         self.local[0] = self._wdot(self.r, self.r)
 
+    def update_alpha(self, bot, top, gathered):
+        """Mirror of sem_cg_update_slab_alpha: finish(1) folded into update."""
+        self.finish(1, gathered)
+        self.update(bot, top)
+
     def result(self):
         st = self.st
         return (self.x, self.history[:st["iters"]].copy(), st["iters"], st["stop"], st["pap"],
@@ -179,8 +184,8 @@ N = 4
 ITERS = 25
 
 
-def _problem():
-    ex, ey, ez = BOX
+def _problem(box=BOX):
+    ex, ey, ez = box
     E = ex * ey * ez
     b_nodes = None  # basis from the golden fixture (pinned to the reference)
     G = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
@@ -191,12 +196,12 @@ def _problem():
     return dx, dxt, T, g, f, b_nodes
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, box=BOX):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        dx, dxt, T, g, f, _ = _problem()
-        ex, ey, ez = BOX
+        dx, dxt, T, g, f, _ = _problem(box)
+        ex, ey, ez = box
         part = SlabPartition(ex, ey, ez, N, world, rank)
         e0, e1 = part.element_range
         comm = SlabComm(part)
@@ -216,19 +221,20 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
-def test_dist_dssum_and_cg_gloo(world):
+@pytest.mark.parametrize("world,box", [(2, BOX), (3, BOX), (4, BOX),
+                                       (8, (2, 2, 8))])  # world 8: one element layer per rank
+def test_dist_dssum_and_cg_gloo(world, box):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, box)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=240) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    dx, dxt, T, g, f, _ = _problem()
+    dx, dxt, T, g, f, _ = _problem(box)
     x_ref, hist_ref, its = O.cg(f, lambda p: O.apply_global(p, g, dx, dxt, T), T, ITERS)
     hists = {r: h for r, _, h, _, _, _ in out}
     for rank, ok_dssum, hist, iters, x, (e0, e1) in out:
