@@ -526,6 +526,7 @@ def run_ours(args, rank, world, local_rank):
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29571")
+            os.environ.setdefault("NCCL_DEBUG", "WARN")  # no version banner on stdout
             dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
         cg_slab1 = bench_cg_weak(sb, dev, 1, 0, args.cg_weak_iters, force_slab=True)
         dist.destroy_process_group()
@@ -689,6 +690,26 @@ def bench_cg(sb, dev, iters):
                     "timed with CUDA events incl. one host sync at the end"}
 
 
+NCCL_LOG = "/tmp/sem_bench_nccl_rankRANK.log"
+
+
+def nccl_summary(rank: int, limit: int = 12) -> list | None:
+    """The lines of this rank's NCCL init report that say how the
+    communicator was built (ranks, transport, NVLS / NVSwitch, channels)."""
+    path = NCCL_LOG.replace("RANK", str(rank))
+    if not os.path.exists(path):
+        return None
+    keys = ("nRanks", "NVLS", "NVLink", "P2P", "Channel", "comm ", "Init COMPLETE", "version")
+    out = []
+    with open(path, errors="replace") as fh:
+        for line in fh:
+            if any(k in line for k in keys):
+                out.append(line.strip()[:200])
+            if len(out) >= limit:
+                break
+    return out
+
+
 def bench_cg_weak(sb, dev, world, rank, iters, force_slab=False):
     """Weak-scaled CG: E=32768 per GPU, p=9, global box factor_elements(32768*G)
     split into z-slabs (dist.py).  G=1 runs the fused single-GPU solver
@@ -741,18 +762,40 @@ def bench_cg_weak(sb, dev, world, rank, iters, force_slab=False):
         ev1.record()
         torch.cuda.synchronize(dev)
         hist_last = float(res.residual_history[-1])
+        graphed = comm.capturable and iters > 2
         path = (f"z-slab partition, {dist.get_backend()} halo (2 ordered P2P steps, interior Ax "
-                "overlapping the first) + rank-ordered all_gather")
+                "overlapping the first) + rank-ordered all_gather"
+                + (", one CUDA graph per iteration" if graphed else ", eager launches"))
+        # per-rank compute / communication breakdown: a short eager run with
+        # CUDA events at the phase boundaries (not the timed solve)
+        from paper_2005_13425_b200.dist import dist_cg_phases
+        k = 10
+        ph = dist_cg_phases(ops, comm, f_l, k)
+        mine = {name: round(ms * 1e3 / k, 2) for name, ms in ph.items()}
+        if world > 1:
+            every = [None] * world
+            dist.all_gather_object(every, mine)
+        else:
+            every = [mine]
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         ms = max_over_ranks(ms, dev)
     per_it = ms / iters
     dofs_total = e_total * n ** 3
     model = perf.model_flops_per_iteration(dofs_total, n) / (per_it * 1e-3)
-    return {"global_box": [ex, ey, ez], "elements_per_gpu": per, "iterations": iters,
-            "ms_per_iteration": per_it, "model_gflops_total": model / 1e9,
-            "model_gflops_per_gpu": model / 1e9 / world, "final_residual": hist_last,
-            "path": path, "timing": "CUDA events, max over ranks"}
+    out = {"global_box": [ex, ey, ez], "elements_per_gpu": per, "iterations": iters,
+           "ms_per_iteration": per_it, "model_gflops_total": model / 1e9,
+           "model_gflops_per_gpu": model / 1e9 / world, "final_residual": hist_last,
+           "path": path, "timing": "CUDA events, max over ranks"}
+    if not (world == 1 and not force_slab):
+        out["phases_us_per_iteration_by_rank"] = every
+        out["phases_note"] = ("eager run of 10 iterations with CUDA events on the compute "
+                              "stream: ax = Ax up to the first exchange, halo = planes + P2P "
+                              "+ overlapped interior Ax, pap = settle + all_gather, update = "
+                              "alpha + r update, rr = all_gather + finish")
+        if world > 1 and rank == 0:
+            out["nccl"] = nccl_summary(rank)
+    return out
 
 
 def main(argv=None):
@@ -779,7 +822,7 @@ def main(argv=None):
     ap.add_argument("--ax-sizes", type=int, default=1, help="also time E=1024/2048 (config 2)")
     ap.add_argument("--cg-weak", type=int, default=1)
     ap.add_argument("--cg-weak-iters", type=int, default=100)
-    ap.add_argument("--cg-slab1", action="store_true",
+    ap.add_argument("--cg-slab1", type=int, default=1,
                     help="also time the multi-GPU slab solver on 1 GPU (NCCL world of 1)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
@@ -801,6 +844,12 @@ def main(argv=None):
         if os.environ.get("SEM_BENCH_SHARE_GPU") == "1":
             dist.init_process_group("gloo")
         else:
+            # NCCL's init report (transport, NVLS, channels) to a per-rank file
+            # that rank 0 summarises in the JSON line (stdout stays clean)
+            if "NCCL_DEBUG" not in os.environ:
+                os.environ["NCCL_DEBUG"] = "INFO"
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV,GRAPH,NVLS")
+                os.environ.setdefault("NCCL_DEBUG_FILE", NCCL_LOG.replace("RANK", str(rank)))
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         return run_ours(args, rank, world, local_rank)
