@@ -275,6 +275,18 @@ int sem_box_geom(double *g, int64_t num_elements, int32_t n, const double *weigh
  * copy that measure_bandwidth times (perf.py:156-203, paper §V). */
 int sem_stream_copy(double *dst, const double *src, int64_t count, sem_stream_t stream);
 
+/* ------------------------------------------------------- L2 residency -- */
+/* Device limits in bytes: persisting-L2 carve-out maximum, access-policy
+ * window maximum, L2 size. */
+int sem_l2_props(int64_t *persist_max, int64_t *window_max, int64_t *l2_bytes);
+/* Mark [base, base+bytes) L2-persisting (hit_ratio of its lines) for kernels
+ * launched into / captured from `stream`; set_aside > 0 sizes the device's
+ * persisting carve-out (clamped).  bytes == 0 clears the window and resets
+ * the persisting lines.  Used by the fused CG (cg.py) to keep r and w in L2
+ * between its launches; no reference counterpart (a B200 residency knob). */
+int sem_l2_window(void *base, int64_t bytes, double hit_ratio, int64_t set_aside,
+                  sem_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

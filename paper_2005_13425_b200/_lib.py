@@ -97,6 +97,8 @@ SIGNATURES = {
     "sem_random_field": (ctypes.c_int, [_vp, _i64, ctypes.c_uint64, _vp]),
     "sem_box_geom": (ctypes.c_int, [_vp, _i64, _i32, _dp, _f64, _vp]),
     "sem_stream_copy": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
+    "sem_l2_props": (ctypes.c_int, [ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "sem_l2_window": (ctypes.c_int, [_vp, _i64, _f64, _i64, _vp]),
 }
 
 _lib = None

@@ -48,12 +48,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     link the shared library."""
     if not force and not _stale():
         return OUT
-    objdir = tempfile.mkdtemp(prefix="libsem_obj_")
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
     # tuning experiments: extra -D definitions (e.g. SEM_NVCC_DEFS="SEM_UPD_MINB=8")
     compile_flags += [f"-D{d}" for d in os.environ.get("SEM_NVCC_DEFS", "").split()]
     if verbose:
         compile_flags += ["-Xptxas", "-v"]
+    # objects are cached per flag set outside the tree (SEM_OBJ_CACHE): a unit
+    # is recompiled when its .cu, any header or the flags changed
+    cache = os.environ.get("SEM_OBJ_CACHE")
+    if cache and not force:
+        import hashlib
+        key = hashlib.sha1(" ".join(compile_flags).encode()).hexdigest()[:12]
+        objdir = os.path.join(cache, key)
+        os.makedirs(objdir, exist_ok=True)
+    else:
+        objdir = tempfile.mkdtemp(prefix="libsem_obj_")
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    headers.append(os.path.join(HERE, "..", "include", "sem.h"))
+    t_hdr = max(os.path.getmtime(h) for h in headers if os.path.exists(h))
     units = [(src, src.replace(".cu", ".o"), []) for src in SOURCES]
     units += [("ax_inst.cu", f"ax_inst{k}.o", [f"-DSEM_AX_GROUP={k}"]) for k in range(AX_GROUPS)]
     units.sort(key=lambda u: u[0] != "ax_inst.cu")  # longest jobs first
@@ -61,6 +73,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src, objname, extra in units:
         obj = os.path.join(objdir, objname)
         objs.append(obj)
+        if os.path.exists(obj) and os.path.getmtime(obj) > max(
+                t_hdr, os.path.getmtime(os.path.join(CSRC, src))):
+            continue
         cmd = [nvcc(), *compile_flags, *extra, "-c", "-o", obj, os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
@@ -72,7 +87,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             "-o", OUT + ".tmp", *objs]
     subprocess.run(link, check=True)
     os.replace(OUT + ".tmp", OUT)
-    shutil.rmtree(objdir, ignore_errors=True)
+    if not (cache and not force):
+        shutil.rmtree(objdir, ignore_errors=True)
     return OUT
 
 

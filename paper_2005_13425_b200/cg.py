@@ -101,9 +101,15 @@ class CgWorkspace:
         topo = as_topology(topo)
         shape = (topo.num_elements, topo.n, topo.n, topo.n)
         self.box = (topo.ex, topo.ey, topo.ez, topo.n)
-        mk = lambda: torch.empty(shape, dtype=torch.float64, device=device)  # noqa: E731
-        self.x, self.r, self.p = mk(), mk(), mk()
-        self.w = torch.empty((2,) + shape, dtype=torch.float64, device=device)
+        # one allocation, [x | p | r | w | w2]: the vectors an iteration
+        # re-reads soonest (r, w; then p) are adjacent, so one L2 access-policy
+        # window can cover them (_l2_window)
+        m = topo.num_elements * topo.n ** 3
+        self._buf = torch.empty(5 * m, dtype=torch.float64, device=device)
+        v = [self._buf[q * m:(q + 1) * m].view(shape) for q in range(3)]
+        self.x, self.p, self.r = v
+        self.w = self._buf[3 * m:].view((2,) + shape)
+        self._m = m
         self.history = torch.zeros(max(1, max_iterations), dtype=torch.float64, device=device)
         self.state = torch.zeros(ctypes_sizeof_state(), dtype=torch.uint8, device=device)
         self.scratch = torch.zeros(int(load().sem_reduce_scratch_bytes()), dtype=torch.uint8,
@@ -142,6 +148,28 @@ class CgWorkspace:
         return sem_cg_state.from_buffer_copy(raw)
 
 
+def _l2_window(ws: CgWorkspace, stream) -> bool:
+    """Keep the vectors an iteration re-reads soonest L2-resident across its
+    launches: an access-policy window over [p | r | w] (SEM_CG_L2 = "rw",
+    "prw" or "off"; SEM_CG_L2_HIT = hit ratio)."""
+    import os
+    mode = os.environ.get("SEM_CG_L2", "off")
+    if mode == "off":
+        return False
+    m8 = ws._m * 8
+    first = {"rw": 2, "prw": 1, "xprw": 0}[mode]
+    base = ws._buf.data_ptr() + first * m8
+    nbytes = (4 - first) * m8
+    hit = float(os.environ.get("SEM_CG_L2_HIT", "1.0"))
+    import ctypes
+    pm, wm, l2 = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    lib = load()
+    check(lib.sem_l2_props(ctypes.byref(pm), ctypes.byref(wm), ctypes.byref(l2)), "L2 props")
+    setaside = int(os.environ.get("SEM_CG_L2_SETASIDE", str(pm.value)))
+    check(lib.sem_l2_window(base, nbytes, hit, setaside, stream), "cg_solve L2 window")
+    return True
+
+
 def ctypes_sizeof_state() -> int:
     import ctypes
     return ctypes.sizeof(sem_cg_state)
@@ -161,6 +189,8 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
     check(lib.sem_cg_init(dv.ptr(f_dev), dv.ptr(ws.x), dv.ptr(ws.r), dv.ptr(ws.p),
                           dv.ptr(ws.state), dv.ptr(ws.history), cfg.max_iterations,
                           float(cfg.tolerance), *box, dv.ptr(ws.scratch), s), "cg_solve init")
+
+    win = _l2_window(ws, s)
 
     def run(k: int):
         # stream looked up at call time: inside graph capture it is the capture stream
@@ -238,6 +268,8 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
                 callback(it, x, r)
             if st.stop:
                 break
+    if win:
+        check(lib.sem_l2_window(None, 0, 0.0, 0, s), "cg_solve L2 window reset")
     if st.stop == 2:
         ppc = float(_glsc3_box_dev(ws.p, ws.p, topo).item())
         raise CgBreakdownError(

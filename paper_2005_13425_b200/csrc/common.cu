@@ -2,6 +2,7 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "sem_common.cuh"
@@ -78,3 +79,61 @@ extern "C" int sem_min_points(void) { return 2; }
 
 extern "C" int64_t sem_fallback_count(void) { return (int64_t)sem::g_fallbacks.load(); }
 extern "C" int sem_max_points(void) { return 16; }
+
+// ------------------------------------------------------- L2 residency --
+// Device L2 persistence limits (bytes): the largest set-aside for persisting
+// lines and the largest access-policy window.
+extern "C" int sem_l2_props(int64_t* persist_max, int64_t* window_max, int64_t* l2_bytes)
+{
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return sem::fail_cuda(e, "sem_l2_props: cudaGetDevice");
+    int pm = 0, wm = 0, l2 = 0;
+    cudaDeviceGetAttribute(&pm, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&wm, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    if (persist_max) *persist_max = pm;
+    if (window_max) *window_max = wm;
+    if (l2_bytes) *l2_bytes = l2;
+    return 0;
+}
+
+// Mark [base, base + bytes) as L2-persisting for kernels launched into
+// `stream` (and kernels captured from it): hit_ratio of the window's lines
+// get the persisting property, the rest stream.  set_aside > 0 sizes the
+// device's persisting carve-out (clamped to the device maximum); bytes == 0
+// clears the window and releases the persisting lines.
+extern "C" int sem_l2_window(void* base, int64_t bytes, double hit_ratio, int64_t set_aside,
+                             sem_stream_t stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = sem::bind_stream_device(s)) return rc;
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return sem::fail_cuda(e, "sem_l2_window: cudaGetDevice");
+    cudaStreamAttrValue v = {};
+    if (bytes > 0) {
+        int pm = 0, wm = 0;
+        cudaDeviceGetAttribute(&pm, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&wm, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        if (set_aside > 0) {
+            const size_t sa = (size_t)std::min<int64_t>(set_aside, (int64_t)pm);
+            if (cudaError_t e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, sa))
+                return sem::fail_cuda(e, "sem_l2_window: cudaDeviceSetLimit");
+        }
+        v.accessPolicyWindow.base_ptr = base;
+        v.accessPolicyWindow.num_bytes = (size_t)std::min<int64_t>(bytes, (int64_t)wm);
+        v.accessPolicyWindow.hitRatio = (float)(hit_ratio < 0 ? 0 : hit_ratio > 1 ? 1 : hit_ratio);
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    } else {
+        v.accessPolicyWindow.num_bytes = 0;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+    }
+    if (cudaError_t e = cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v))
+        return sem::fail_cuda(e, "sem_l2_window: cudaStreamSetAttribute");
+    if (bytes <= 0) {
+        if (cudaError_t e = cudaCtxResetPersistingL2Cache())
+            return sem::fail_cuda(e, "sem_l2_window: cudaCtxResetPersistingL2Cache");
+    }
+    return 0;
+}
