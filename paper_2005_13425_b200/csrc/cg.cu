@@ -27,6 +27,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 
 #ifndef SEM_UPD_MINB
 #define SEM_UPD_MINB 6
@@ -301,6 +302,19 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         if (blockIdx.x == 0 && threadIdx.x == 0) fin_pap(st, pap_s);
         if (pap_s <= 0.0) return;  // breakdown (block 0 set stop = 2)
         alpha = ldexp(st->rtz, 2 * pap_scale_exp(st->rtz)) / pap_s;
+    } else if (gathered != nullptr) {
+        // single GPU, settle folded in: every CTA sums the Ax launch's
+        // per-CTA <p, A p> partials in one fixed order (so every CTA derives
+        // the same alpha bit for bit) -- no settle launch between the two
+        // streaming kernels; block 0 records the state
+        __shared__ double pap_sh;
+        const double t = settle_sum<RT>(gathered, nranks);
+        if (threadIdx.x == 0) pap_sh = t;
+        __syncthreads();
+        const double pap_s = pap_sh;
+        if (blockIdx.x == 0 && threadIdx.x == 0) fin_pap(st, pap_s);
+        if (pap_s <= 0.0) return;  // breakdown (block 0 set stop = 2)
+        alpha = ldexp(st->rtz, 2 * pap_scale_exp(st->rtz)) / pap_s;
     } else {
         alpha = st->alpha;
     }
@@ -331,6 +345,231 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         if (DIST) st->local_sum = t[0];
         else fin_rr(st, t[0], history);
     });
+}
+
+// Element-granular form of the same iteration tail ("cube" update): each
+// CTA holds SLOTS elements; for each, the element's own w and the copies its
+// 26 neighbours hold of its boundary nodes are gathered into an extended
+// (n+2)^3 cube in shared memory by asynchronous copies (cp.async: nothing
+// is staged in registers, so every copy of the element is in flight at
+// once), then one thread per (j, k) row sums its points' copies from the
+// cube in ascending element order -- z, then y, then x, the order of
+// dssum_row, so the assembled values are bit-identical -- and updates its r
+// row.  The row kernel issues a row's loads only after the previous row's
+// arithmetic (latency-bound at small E); here the fill of a whole element
+// is one round trip.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// cube index (0 .. N+1) of the copies of local index l along y or z, in
+// ascending element order (axis_copies)
+template <int N>
+__device__ __forceinline__ void cube_copies(int ec, int l, int ecount, int& cnt, int& h0, int& h1)
+{
+    if (l == 0 && ec > 0) {
+        cnt = 2; h0 = 0; h1 = 1;
+    } else if (l == N - 1 && ec < ecount - 1) {
+        cnt = 2; h0 = N; h1 = N + 1;
+    } else {
+        cnt = 1; h0 = l + 1; h1 = l + 1;
+    }
+}
+
+template <int N>
+struct CubeCfg {
+    static constexpr int NN = N * N, NNN = N * N * N;
+    // per slot (doubles): W own w [n^3] | R r [n^3] | ZF z-face planes of the
+    // z neighbours [2][n^2] | YF y-face rows of the y neighbours [2][n][n] |
+    // ED edge rows of the yz-diagonal neighbours [4][n] | XS x-neighbour
+    // copies of the end nodes of every cube row [2][n+2][n+2]
+    static constexpr int OW = 0, OR = NNN, OZ = 2 * NNN, OY = OZ + 2 * NN, OE = OY + 2 * NN,
+                         OX = OE + 4 * N, XSP = (N + 2) * (N + 2);
+    static constexpr int SLOT_D = (OX + 2 * XSP + 1) / 2 * 2;
+    static constexpr int SLOTS = 1;
+    static constexpr int THREADS = ((SLOTS * NN + 31) / 32) * 32;
+    static constexpr size_t SMEM = sizeof(double) * (size_t)SLOTS * SLOT_D + 16;  // + mbarrier
+    static constexpr int BY_SMEM = (int)((228 * 1024) / (SMEM + 1024));
+    static constexpr int BY_THREADS = 1024 / THREADS;
+    static constexpr int MINB = BY_SMEM < BY_THREADS ? BY_SMEM : BY_THREADS;
+};
+
+// cube row (kk, jj) of a slot: its N values
+template <int N>
+__device__ __forceinline__ const double* cube_row(const double* S, int kk, int jj)
+{
+    using C = CubeCfg<N>;
+    const bool zin = kk >= 1 && kk <= N, yin = jj >= 1 && jj <= N;
+    if (zin && yin) return S + C::OW + (kk - 1) * C::NN + (jj - 1) * N;
+    if (zin) return S + C::OY + (jj == 0 ? 0 : C::NN) + (kk - 1) * N;
+    if (yin) return S + C::OZ + (kk == 0 ? 0 : C::NN) + (jj - 1) * N;
+    return S + C::OE + ((kk == 0 ? 0 : 2) + (jj == 0 ? 0 : 1)) * N;
+}
+
+// x-neighbour copies (lo, hi) of the end nodes of cube row (kk, jj) whose
+// source row is (j2, k2) of element e2
+template <int N>
+__device__ __forceinline__ void fill_row_ends(double* S, const double* __restrict__ w, int64_t e2,
+                                              int j2, int k2, int kk, int jj, bool lo, bool hi)
+{
+    using C = CubeCfg<N>;
+    const double* src = w + e2 * C::NNN + (k2 * N + j2) * N;
+    if (lo) cp_async8(S + C::OX + kk * (N + 2) + jj, src - C::NNN + (N - 1));
+    if (hi) cp_async8(S + C::OX + C::XSP + kk * (N + 2) + jj, src + C::NNN);
+}
+
+template <int N>
+__global__ void __launch_bounds__(CubeCfg<N>::THREADS, CubeCfg<N>::MINB)
+cg_update_cube_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t E,
+                      BoxFlat bf, sem_cg_state* st, double* history, ReduceScratch* rs)
+{
+    using C = CubeCfg<N>;
+    static_assert(N % 2 == 0, "bulk copies of n-double rows need even n");
+    constexpr int NN = C::NN, NNN = C::NNN;
+    extern __shared__ __align__(16) double smem[];
+    double* S = smem;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::SLOT_D);
+    const int tid = threadIdx.x;
+    if (tid == 0) mbar_init(bar, 1);
+    __syncthreads();
+    griddep_wait();
+    if (st->stop) return;
+    const double nalpha = -st->alpha;
+    const Box& b = bf.b;
+    const int q = tid, j = q % N, k = q / N;
+    const bool lane_ok = q < NN;
+    const int64_t ys = b.ex, zs = (int64_t)b.ex * b.ey;
+    double acc = 0.0;
+    unsigned phase = 0;
+    for (int64_t e = blockIdx.x; e < E; e += gridDim.x, phase ^= 1u) {
+        const ElemCoord c = elem_coord_fast((uint32_t)e, bf);
+        const bool zlo = c.iz > 0, zhi = c.iz < b.ez - 1, ylo = c.iy > 0, yhi = c.iy < b.ey - 1;
+        const bool lo = c.ix > 0, hi = c.ix < b.ex - 1;
+        // warp 0: the bulk copies (TMA engine), one per lane
+        if (tid < 32) {
+            unsigned bytes = 2u * NNN * 8 + (zlo + zhi) * NN * 8 + (ylo + yhi) * NN * 8 +
+                             ((zlo + zhi) * (ylo + yhi)) * N * 8;
+            if (tid == 0) mbar_expect_tx(bar, bytes);
+            __syncwarp();
+            const double* we = w + e * NNN;
+            // copy index: 0 W, 1 R, 2/3 z planes, 4..4+2N-1 y rows, then 4 edges
+            for (int cidx = tid; cidx < 4 + 2 * N + 4; cidx += 32) {
+                if (cidx == 0) bulk_g2s(S + C::OW, we, NNN * 8, bar);
+                else if (cidx == 1) bulk_g2s(S + C::OR, r + e * NNN, NNN * 8, bar);
+                else if (cidx == 2) { if (zlo) bulk_g2s(S + C::OZ, we - zs * NNN + (N - 1) * NN, NN * 8, bar); }
+                else if (cidx == 3) { if (zhi) bulk_g2s(S + C::OZ + NN, we + zs * NNN, NN * 8, bar); }
+                else if (cidx < 4 + 2 * N) {
+                    const int side = (cidx - 4) / N, kr = (cidx - 4) % N;
+                    if (side == 0 ? ylo : yhi)
+                        bulk_g2s(S + C::OY + side * NN + kr * N,
+                                 we + (side == 0 ? -ys : ys) * NNN + kr * NN + (side == 0 ? (N - 1) * N : 0),
+                                 N * 8, bar);
+                } else {
+                    const int d = cidx - 4 - 2 * N, zsd = d >> 1, ysd = d & 1;
+                    if ((zsd == 0 ? zlo : zhi) && (ysd == 0 ? ylo : yhi))
+                        bulk_g2s(S + C::OE + d * N,
+                                 we + ((zsd == 0 ? -zs : zs) + (ysd == 0 ? -ys : ys)) * NNN +
+                                     (zsd == 0 ? (N - 1) * NN : 0) + (ysd == 0 ? (N - 1) * N : 0),
+                                 N * 8, bar);
+                }
+            }
+        }
+        // every thread: the x-neighbour copies of its row's end nodes (and
+        // of the y / z / yz neighbour rows it sums)
+        int dy = 0, dz = 0;
+        if (lane_ok) {
+            dy = (j == 0 && ylo) ? -1 : ((j == N - 1 && yhi) ? 1 : 0);
+            dz = (k == 0 && zlo) ? -1 : ((k == N - 1 && zhi) ? 1 : 0);
+            const int jj = dy < 0 ? 0 : N + 1, kk = dz < 0 ? 0 : N + 1;
+            const int j2 = dy < 0 ? N - 1 : 0, k2 = dz < 0 ? N - 1 : 0;
+            fill_row_ends<N>(S, w, e, j, k, k + 1, j + 1, lo, hi);
+            if (dy != 0) fill_row_ends<N>(S, w, e + dy * ys, j2, k, k + 1, jj, lo, hi);
+            if (dz != 0) fill_row_ends<N>(S, w, e + dz * zs, j, k2, kk, j + 1, lo, hi);
+            if (dy != 0 && dz != 0) fill_row_ends<N>(S, w, e + dy * ys + dz * zs, j2, k2, kk, jj, lo, hi);
+        }
+        cp_async_wait_all();
+        if (tid == 0) mbar_wait(bar, phase);  // the others wait at the barrier
+        __syncthreads();
+        if (lane_ok) {
+            Row<N> rw;
+            rw.e = e;
+            rw.jk = q;
+            rw.j = j;
+            rw.k = k;
+            rw.c = c;
+            const int gz = c.iz + b.gz0;
+            rw.yz_inner = axis_interior<N>(c.iy, j, b.ey) && axis_interior<N>(gz, k, b.ez_global);
+            const int m = axis_mult<N>(c.iy, j, b.ey) * axis_mult<N>(gz, k, b.ez_global);
+            rw.inv_myz = m == 1 ? 1.0 : (m == 2 ? 0.5 : 0.25);
+            rw.x_lo_in = lo;
+            rw.x_hi_in = hi;
+            int cy, y0, y1, cz, z0, z1;
+            cube_copies<N>(c.iy, j, b.ey, cy, y0, y1);
+            cube_copies<N>(c.iz, k, b.ez, cz, z0, z1);
+            double v[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) v[i] = 0.0;
+#pragma unroll
+            for (int zc = 0; zc < 2; ++zc) {
+                if (zc >= cz) break;
+#pragma unroll
+                for (int yc = 0; yc < 2; ++yc) {
+                    if (yc >= cy) break;
+                    const int kk = zc ? z1 : z0, jj = yc ? y1 : y0;
+                    double s[N];
+                    stack_row_ld<N>(cube_row<N>(S, kk, jj), s);
+                    const double xl = lo ? S[C::OX + kk * (N + 2) + jj] : 0.0;
+                    const double xh = hi ? S[C::OX + C::XSP + kk * (N + 2) + jj] : 0.0;
+                    v[0] = lo ? add_rn(add_rn(v[0], xl), s[0]) : add_rn(v[0], s[0]);
+#pragma unroll
+                    for (int i = 1; i < N - 1; ++i) v[i] = add_rn(v[i], s[i]);
+                    v[N - 1] = hi ? add_rn(add_rn(v[N - 1], s[N - 1]), xh) : add_rn(v[N - 1], s[N - 1]);
+                }
+            }
+            double rv[N];
+            stack_row_ld<N>(S + C::OR + q * N, rv);
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                rv[i] = add_rn(rv[i], mul_rn(nalpha, mul_rn(v[i], row_mask<N>(rw, i))));
+                acc += mul_rn(mul_rn(rv[i], rv[i]), row_inv_mult<N>(rw, i));
+            }
+            store_row<N>(r + e * NNN + q * N, rv);
+        }
+        __syncthreads();  // the slot is refilled for the next element
+    }
+    griddep_launch();
+    const double vals[1] = {acc};
+    reduce_publish_and_finish<1, C::THREADS>(vals, rs,
+                                             [&](const double (&t)[1]) { fin_rr(st, t[0], history); });
+}
+
+// cube-update grid: one resident wave of CTAs, a function of E and n only
+// (so the reduction tree is fixed)
+template <int N>
+static unsigned upd_cube_grid(int64_t E)
+{
+    using C = CubeCfg<N>;
+    static const int cap = getenv("SEM_CG_EUPD_BLOCKS") ? atoi(getenv("SEM_CG_EUPD_BLOCKS")) : 0;
+    const int64_t nb = E;
+    int64_t blocks = std::min<int64_t>(nb, (int64_t)C::MINB * 148);
+    if (cap > 0 && cap <= kReduceBlocksMax) blocks = std::min<int64_t>(nb, cap);
+    return (unsigned)(blocks > 0 ? blocks : 1);
+}
+
+// update form (SEM_CG_UPD_ELEM: 1 element kernel, 0 row kernel)
+static int upd_elem()
+{
+    static const int k = getenv("SEM_CG_UPD_ELEM") ? atoi(getenv("SEM_CG_UPD_ELEM")) : 0;
+    return k;
 }
 
 template <int N, bool DIST>
@@ -364,6 +603,14 @@ cg_settle_kernel(const double* __restrict__ partials, int count, sem_cg_state* s
     else fin_phase(st, PH, tot, history);
 }
 
+// <p, A p> settle: 1 (default) a one-block settle launch after the Ax
+// launch, 0 folded into every update CTA (SEM_CG_SETTLE)
+static int settle_launch()
+{
+    static const int k = getenv("SEM_CG_SETTLE") ? atoi(getenv("SEM_CG_SETTLE")) : 1;
+    return k;
+}
+
 // tuning hook SEM_CG_FIN (0: fused reductions, 1: both deferred, 2: the Ax
 // reduction deferred only)
 static int fin_mode()
@@ -395,6 +642,34 @@ cg_finalize_kernel(double* __restrict__ x, const double* __restrict__ p, int64_t
 
 __global__ void cg_clear_pending_kernel(sem_cg_state* st) { st->x_pending = 0; }
 
+// launch of the cube update (even n only: n-double rows are bulk-copied)
+template <int N>
+static int launch_cube_update(const double* w, double* r, int64_t E, const Box& bx,
+                              sem_cg_state* st, double* history, ReduceScratch* rs, cudaStream_t s,
+                              bool pdl)
+{
+    if constexpr (N % 2 != 0) {
+        set_error("cube update: odd n");
+        return SEM_E_INVALID;
+    } else {
+        using UC = CubeCfg<N>;
+        auto kern = cg_update_cube_kernel<N>;
+        static std::atomic<uint64_t> configured{0};
+        int dev = 0;
+        if (cudaError_t e = cudaGetDevice(&dev)) return fail_cuda(e, "cube update: cudaGetDevice");
+        const uint64_t bit = 1ull << (dev & 63);
+        if (!(configured.load(std::memory_order_acquire) & bit)) {
+            if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)UC::SMEM))
+                return fail_cuda(e, "cube update: attribute");
+            configured.fetch_or(bit, std::memory_order_release);
+        }
+        cudaError_t e = launch_k(kern, dim3(upd_cube_grid<N>(E)), dim3(UC::THREADS), UC::SMEM, s, pdl,
+                                 w, r, E, make_box_flat(bx), st, history, rs);
+        return e == cudaSuccess ? 0 : fail_cuda(e, "cg update (cube) kernel");
+    }
+}
+
 template <int N>
 static int cg_run_n(const double* g, const double* dx, double* x, double* r, double* p,
                     double* w, double* w2, sem_cg_state* st, double* history, int iters,
@@ -419,14 +694,17 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
     for (int it = 0; it < iters; ++it) {
         if (cudaError_t e = mark(3 * it)) return fail_cuda(e, "sem_cg_run: event");
         if (int rc = ax_cg_dispatch(g, dx, w, E, N, a, 2, s)) return rc;
-        if (defer_ax) {
+        const bool fold = defer_ax && !defer && !settle_launch() && !upd_elem();
+        if (defer_ax && !fold) {
             if (int rc = chk(launch_k(cg_settle_kernel<kPhasePap>, dim3(1), dim3(kSettleThreads), 0, s,
                                       pdl, (const double*)w2, (int)ax_grid, st, history, 0),
                              "cg settle (pap)"))
                 return rc;
         }
         if (cudaError_t e = mark(3 * it + 1)) return fail_cuda(e, "sem_cg_run: event");
-        if (defer) {
+        if (N % 2 == 0 && upd_elem() && !defer) {
+            if (int rc = launch_cube_update<N>(w, r, E, bx, st, history, rs, s, pdl)) return rc;
+        } else if (defer) {
             const unsigned ug = rt256 ? upd_grid<N, 256>(E) : upd_grid<N>(E);
             if (int rc = chk(rt256 ? launch_k(cg_update2_kernel<N, false, 256>, dim3(ug), dim3(256), 0, s,
                                               pdl, (const double*)w, r, E, make_box_flat(bx), st,
@@ -443,14 +721,16 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
                              "cg settle (rr)"))
                 return rc;
         } else {
+            const double* gath = fold ? (const double*)w2 : (const double*)nullptr;
+            const int ng = fold ? (int)ax_grid : 0;
             if (int rc = chk(rt256 ? launch_k(cg_update2_kernel<N, false, 256>, dim3(upd_grid<N, 256>(E)),
                                               dim3(256), 0, s, pdl, (const double*)w, r, E,
                                               make_box_flat(bx), st, history, rs,
-                                              (const double*)nullptr, (const double*)nullptr, false, (const double*)nullptr, 0)
+                                              (const double*)nullptr, (const double*)nullptr, false, gath, ng)
                                    : launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
                                               dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E,
                                               make_box_flat(bx), st, history, rs,
-                                              (const double*)nullptr, (const double*)nullptr, false, (const double*)nullptr, 0),
+                                              (const double*)nullptr, (const double*)nullptr, false, gath, ng),
                              "cg update kernel"))
                 return rc;
         }

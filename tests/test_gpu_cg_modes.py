@@ -8,7 +8,9 @@ in its own subprocess):
                  2 (default) the settle and update launches only;
   * SEM_CG_AX_CFG 0 (default, GMODE 4: p / r / x / g bulk-copied before the
                  scalars are read) vs 4 (metric only staged, p / r / x via
-                 registers).
+                 registers);
+  * SEM_CG_UPD_ELEM 1 element-granular update (extended cube in shared
+                 memory) vs 0 the row kernel.
 
 Every mode is deterministic run to run; modes with the same reduction trees
 (PDL, Ax staging) agree bit-for-bit with the default, and all agree with the
@@ -53,6 +55,10 @@ MODES = {
     "pdl0": {"SEM_CG_PDL": "0"},
     "pdl1": {"SEM_CG_PDL": "1"},
     "axcfg4": {"SEM_CG_AX_CFG": "4"},
+    "updrow": {"SEM_CG_UPD_ELEM": "0"},
+    "updelem": {"SEM_CG_UPD_ELEM": "1"},
+    "settle0": {"SEM_CG_SETTLE": "0"},
+    "settle1": {"SEM_CG_SETTLE": "1"},
 }
 
 
