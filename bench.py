@@ -421,9 +421,14 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(3):
             graph.replay()
     torch.cuda.synchronize(dev)
-    # a warm burst of >= --warm-ms of graph-replayed applies runs right before
-    # every timed window (after the clock sampler is delivering), so the
-    # window opens on a GPU that is already streaming at its clocks
+    # a warm burst of --warm-ms of graph-replayed applies runs right before
+    # every timed window (after the clock sampler is delivering) and the
+    # window's launches queue straight behind it (no host sync), so the window
+    # opens on a GPU that is already streaming.  10 ms: long enough that the
+    # graph is resident and HBM streaming, short of the 1000 W power cap --
+    # tools/warm_ab.sh (profiles/r02_headline_warm_ab.txt): 10 ms / no sync
+    # 40.1-40.2 us, 40 ms / sync 40.7-41.0 us, 100 ms 44.4-45.8 us (power
+    # capped: the regime the `sustained` key reports)
     warm_steps = max(1, int(args.warm_ms * 1e-3 / 41e-6))
 
     def timed_region(soak: float):
@@ -511,6 +516,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- secondary: Ax at the paper's other sizes (BASELINE config 2) ----
     ax_sizes = bench_ax_sizes(sb, dev, basis, stream) if (rank == 0 and args.ax_sizes) else None
+    psweep = bench_psweep(sb, dev) if (rank == 0 and world == 1 and args.psweep) else None
 
     # ---- secondary: full Nekbone CG, 100 iterations (BASELINE config 4) ----
     cg = None
@@ -580,6 +586,8 @@ def run_ours(args, rank, world, local_rank):
         }
         if ax_sizes is not None:
             line["ax_e1024_e2048_p9"] = ax_sizes
+        if psweep is not None:
+            line["ax_psweep_e4096"] = psweep
         if cg is not None:
             line["cg_e4096_p9"] = cg
         if cg_weak is not None:
@@ -590,10 +598,79 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
-def bench_ax_sizes(sb, dev, basis, stream, steps=400):
-    """Ax at E = 1024 and 2048 (p = 9): enough rotating input sets that every
-    step streams from HBM (sets x 64 B x E n^3 >= 2 x L2), CUDA-graph
-    replays timed with CUDA events (burst clocks: a short region)."""
+def _graph_us(dev, launch, count, total):
+    """Device microseconds per launch: `count` launches (launch(i) enqueues
+    the i-th on the current stream) captured in one CUDA graph, a warm burst
+    of replays, then ceil(total / count) replays timed with CUDA events --
+    the headline's protocol (no stream-launch gaps, burst clocks)."""
+    import torch
+    graph, side = torch.cuda.CUDAGraph(), torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for i in range(2):
+            launch(i)
+        with torch.cuda.graph(graph, stream=side):
+            for i in range(count):
+                launch(i)
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize(dev)
+    reps = max(1, -(-total // count))
+    stream = torch.cuda.current_stream(dev)
+    best = None
+    for _ in range(2):
+        for _ in range(max(1, reps // 2)):  # warm burst
+            graph.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        us = e0.elapsed_time(e1) * 1e3 / (reps * count)
+        best = us if best is None else min(best, us)
+    return best
+
+
+def _ax_sets(sb, dev, E, n, seed):
+    """Enough rotating (u, g, w) sets that the rotation exceeds 3x L2 (every
+    apply streams from HBM where the sizes allow; at most 8 sets)."""
+    import torch
+    per = ax_bytes(E, n)
+    nsets = min(8, max(2, -(-3 * 126 * 2 ** 20 // per)))
+    sets = []
+    for s_ in range(nsets):
+        u = sb.random_field(E, n, seed + s_, device=dev)
+        g = sb.random_field(6 * E, n, seed + 100 + s_, device=dev).reshape(E, 6, n, n, n)
+        sets.append((u, g, torch.empty_like(u)))
+    return sets
+
+
+def _copy_us(dev, nbytes, nsets, count, total):
+    """Same-bytes reference: sem_stream_copy moving nbytes per launch (half
+    read, half written), rotating over nsets buffer pairs, same protocol."""
+    import torch
+    from paper_2005_13425_b200._lib import load
+    lib = load()
+    half = nbytes // 16
+    bufs = [(torch.ones(half, dtype=torch.float64, device=dev),
+             torch.empty(half, dtype=torch.float64, device=dev)) for _ in range(nsets)]
+
+    def launch(i):
+        src, dst = bufs[i % nsets]
+        rc = lib.sem_stream_copy(dst.data_ptr(), src.data_ptr(), half,
+                                 torch.cuda.current_stream(dev).cuda_stream)
+        assert rc == 0, "sem_stream_copy"
+    us = _graph_us(dev, launch, count, total)
+    del bufs
+    return us
+
+
+def bench_ax_sizes(sb, dev, basis, stream, steps=600):
+    """Ax at E = 1024 and 2048 (p = 9, BASELINE config 2): rotating input
+    sets (>= 3x L2), graph-replayed back-to-back applies like the headline,
+    with a same-bytes copy timed the same way beside each (at these sizes
+    launch ramp and drain are a visible share of a ~10-20 us kernel, for a
+    data mover as much as for Ax)."""
     import torch
     from paper_2005_13425_b200.kernels import apply_ax_into
     from paper_2005_13425_b200.perf import measured_peaks
@@ -601,36 +678,46 @@ def bench_ax_sizes(sb, dev, basis, stream, steps=400):
     hbm = float(measured_peaks(ROOT)["hbm_gbs"])
     out = {}
     for E in (1024, 2048):
-        nsets = max(2, -(-2 * 126 * 2 ** 20 // ax_bytes(E, n)))
-        sets = []
-        for s_ in range(nsets):
-            u = sb.random_field(E, n, 100 + s_, device=dev)
-            g = sb.random_field(6 * E, n, 200 + s_, device=dev).reshape(E, 6, n, n, n)
-            sets.append((u, g, torch.empty_like(u)))
-        for i in range(2 * nsets):
-            apply_ax_into(*sets[i % nsets][:2], basis, sets[i % nsets][2])
-        torch.cuda.synchronize(dev)
-        # one apply per input set captured in a CUDA graph (a 10 us kernel
-        # would otherwise wait on the Python launch path)
-        graph, side = torch.cuda.CUDAGraph(), torch.cuda.Stream(dev)
-        side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side), torch.cuda.graph(graph, stream=side):
-            for u, g, w in sets:
-                apply_ax_into(u, g, basis, w)
-        torch.cuda.current_stream(dev).wait_stream(side)
-        graph.replay()
-        torch.cuda.synchronize(dev)
-        reps = max(1, steps // nsets)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
-            graph.replay()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        us = e0.elapsed_time(e1) * 1e3 / (reps * nsets)
+        sets = _ax_sets(sb, dev, E, n, 100)
+        nsets = len(sets)
+        count = nsets * max(1, 60 // nsets)
+        us = _graph_us(dev, lambda i: apply_ax_into(*sets[i % nsets][:2], basis, sets[i % nsets][2]),
+                       count, steps)
+        cus = _copy_us(dev, ax_bytes(E, n), nsets, count, steps)
         out[f"E{E}"] = {"us_per_apply": us, "gflops": ax_flops(E, n) / us / 1e3,
-                        "hbm_frac": ax_bytes(E, n) / (us * 1e3) / hbm, "input_sets": nsets}
+                        "hbm_frac": ax_bytes(E, n) / (us * 1e3) / hbm, "input_sets": nsets,
+                        "same_bytes_copy_us": cus, "frac_of_same_bytes_copy": cus / us}
         del sets
+        torch.cuda.empty_cache()
+    return out
+
+
+def bench_psweep(sb, dev, steps=300):
+    """BASELINE config 3: the tuned default Ax for every n = 2..16 at
+    E = 4096, same protocol, with the same-bytes copy beside each n (for
+    n <= 6 the rotation fits in L2 and a ~2-10 us launch is ramp-bound: the
+    copy of the same bytes is the roofline that applies there)."""
+    import torch
+    from paper_2005_13425_b200.kernels import apply_ax_into
+    from paper_2005_13425_b200.perf import measured_peaks
+    hbm = float(measured_peaks(ROOT)["hbm_gbs"])
+    E = 4096
+    out = {}
+    for n in range(2, 17):
+        basis = sb.build_basis(n)
+        sets = _ax_sets(sb, dev, E, n, 700)
+        nsets = len(sets)
+        count = nsets * max(1, 30 // nsets)
+        us = _graph_us(dev, lambda i: apply_ax_into(*sets[i % nsets][:2], basis, sets[i % nsets][2]),
+                       count, steps)
+        cus = _copy_us(dev, ax_bytes(E, n), nsets, count, steps)
+        out[str(n)] = {"us_per_apply": round(us, 3), "gflops": round(ax_flops(E, n) / us / 1e3, 1),
+                       "hbm_frac": round(ax_bytes(E, n) / (us * 1e3) / hbm, 4),
+                       "same_bytes_copy_us": round(cus, 3),
+                       "frac_of_same_bytes_copy": round(cus / us, 4),
+                       "rotation_bytes": nsets * ax_bytes(E, n)}
+        del sets
+        torch.cuda.empty_cache()
     return out
 
 
@@ -809,9 +896,9 @@ def main(argv=None):
                     help="seconds of load before the `sustained` timed region")
     ap.add_argument("--graph-steps", type=int, default=50,
                     help="applies per captured CUDA graph in the timed loop (0: eager launches)")
-    ap.add_argument("--warm-ms", type=float, default=40.0,
+    ap.add_argument("--warm-ms", type=float, default=10.0,
                     help="milliseconds of graph-replayed applies right before each timed window")
-    ap.add_argument("--warm-sync", type=int, default=1,
+    ap.add_argument("--warm-sync", type=int, default=0,
                     help="synchronize between the warm burst and the timed window")
     ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -820,6 +907,7 @@ def main(argv=None):
                     help="CG iterations timed on the CPU beside cg_e4096_p9")
     ap.add_argument("--cg", type=int, default=1)
     ap.add_argument("--ax-sizes", type=int, default=1, help="also time E=1024/2048 (config 2)")
+    ap.add_argument("--psweep", type=int, default=1, help="also time n=2..16 at E=4096 (config 3)")
     ap.add_argument("--cg-weak", type=int, default=1)
     ap.add_argument("--cg-weak-iters", type=int, default=100)
     ap.add_argument("--cg-slab1", type=int, default=1,

@@ -511,7 +511,10 @@ static int launch_split(const double* u, const double* g, const double* dx, doub
 // the CTA's own element bulk-prefetched into L2 at start (+10..30%); n = 15,
 // 16 with the B stack aliasing U (profiles/r01_ax_row_stride.txt: 171 -> 163
 // and 185 -> 182 us).
-constexpr int kDefaultVariant[17] = {0, 0, 8, 5, 26, 34, 38, 34, 41, 34, 34, 41, 57, 55, 59, 62, 61};
+// Round 2 (two full sweeps, tools/gpu_psweep.sh, profiles/r02_ax_psweep.txt):
+// n = 2 -> 10, 4 -> 17 (-21%: 3.9 vs 5.0 us), 7 -> 40, 8 -> 40, 9 -> 41
+// (1.6-3.1%, the same winner in both sweeps).
+constexpr int kDefaultVariant[17] = {0, 0, 10, 5, 17, 34, 38, 40, 40, 41, 34, 41, 57, 55, 59, 62, 61};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,

@@ -49,12 +49,50 @@ def time_variant(sets, basis, variant, reps):
     return e0.elapsed_time(e1) / reps
 
 
+def time_copy(nbytes, nsets, reps):
+    """Same-bytes reference: sem_stream_copy of nbytes/2 read + nbytes/2
+    written per launch, rotating over nsets buffer pairs, graph-timed like
+    the Ax launches (the size-matched copy roofline: L2-resident and
+    launch-bound regimes included)."""
+    lib = load()
+    half = nbytes // 2 // 8
+    bufs = [(torch.empty(half, dtype=torch.float64, device="cuda").fill_(1.0),
+             torch.empty(half, dtype=torch.float64, device="cuda")) for _ in range(nsets)]
+
+    def run(i):
+        src, dst = bufs[i % nsets]
+        rc = lib.sem_stream_copy(dst.data_ptr(), src.data_ptr(), half,
+                                 torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(3):
+            run(i)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for i in range(reps):
+            run(i)
+    graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", default="10")
     ap.add_argument("--E", default="4096")
     ap.add_argument("--variants", default="all")
     ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--copy", action="store_true", help="also time a same-bytes copy")
+    ap.add_argument("--repeat", type=int, default=1, help="timings per variant (best kept)")
     args = ap.parse_args()
     hbm = float(measured_peaks(ROOT)["hbm_gbs"])
     lib = load()
@@ -76,7 +114,7 @@ def main():
                                basis.diff, basis.diff_t)
             for v in variants:
                 try:
-                    ms = time_variant(sets, basis, v, args.reps)
+                    ms = min(time_variant(sets, basis, v, args.reps) for _ in range(args.repeat))
                 except Exception as exc:  # noqa: BLE001
                     print(json.dumps({"n": n, "E": E, "variant": v, "error": str(exc)}))
                     continue
@@ -88,6 +126,12 @@ def main():
                                   "gflops": round(E * n ** 3 * (12 * n + 15) / (ms * 1e-3) / 1e9, 1),
                                   "gbs": round(gbs, 1), "frac": round(gbs / hbm, 4),
                                   "rel_err": err}), flush=True)
+            if args.copy:
+                cms = min(time_copy(per_set, nsets, args.reps) for _ in range(args.repeat))
+                cgbs = per_set / (cms * 1e-3) / 1e9
+                print(json.dumps({"n": n, "E": E, "what": "same-bytes copy", "us": round(cms * 1e3, 2),
+                                  "gbs": round(cgbs, 1), "frac": round(cgbs / hbm, 4),
+                                  "sets": nsets}), flush=True)
             del sets
             torch.cuda.empty_cache()
 
