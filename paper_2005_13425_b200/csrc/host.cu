@@ -137,9 +137,11 @@ extern "C" int sem_ax_host(const double* u_host, const double* g, const double* 
     const int nchunks = chunk_schedule(num_elements, chunk_elements, sizes);
     cudaError_t err;
     // the copy streams start after everything already queued on `stream`
+    // (only the copy streams this mode uses join: inside CUDA-graph capture a
+    // stream that waits on the capture and never rejoins it is an error)
     err = cudaEventRecord(P->ev[0], s);
-    if (err == cudaSuccess) err = cudaStreamWaitEvent(P->s_in, P->ev[0], 0);
-    if (err == cudaSuccess) err = cudaStreamWaitEvent(P->s_out, P->ev[0], 0);
+    if (err == cudaSuccess && !zc_in) err = cudaStreamWaitEvent(P->s_in, P->ev[0], 0);
+    if (err == cudaSuccess && !zc_out) err = cudaStreamWaitEvent(P->s_out, P->ev[0], 0);
     if (err != cudaSuccess) return fail_cuda(err, "sem_ax_host: ordering");
     int64_t e0 = 0;
     for (int c = 0; c < nchunks; ++c) {
