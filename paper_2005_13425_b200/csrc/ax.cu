@@ -92,5 +92,5 @@ extern "C" int sem_ax(const double* u, const double* g, const double* dx,
 
 extern "C" int sem_ax_num_variants(int32_t n)
 {
-    return (n >= 2 && n <= 16) ? 71 : 0;
+    return (n >= 2 && n <= 16) ? 76 : 0;
 }

@@ -79,7 +79,8 @@ __device__ __forceinline__ void half_k_wt(const DParamP<N>& D, const double* UT,
 template <int N, int MINB, int PD, bool FOLD>
 __global__ void __launch_bounds__(HalfCfg<N>::THREADS, MINB)
 ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
-               double* __restrict__ w, int64_t num_elements, const DParamP<N> D)
+               double* __restrict__ w, int64_t num_elements, const DParamP<N> D,
+               int64_t uahead = 0)
 {
     using C = HalfCfg<N>;
     constexpr int NN = C::NN, NNN = C::NNN, KH = C::KH, LSU = C::LSU, LSA = C::LSA,
@@ -100,6 +101,10 @@ ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
     if (tid == 0) {  // the whole element streams into L2 at once
         prefetch_l2_bulk(u, e * NNN * 8, (e + 1) * NNN * 8, num_elements * NNN * 8);
         prefetch_l2_bulk(g, e * 6 * NNN * 8, (e + 1) * 6 * NNN * 8, num_elements * 6 * NNN * 8);
+        // and the u block of the element a resident wave later (uahead > 0)
+        if (uahead > 0 && e + uahead < num_elements)
+            prefetch_l2_bulk(u, (e + uahead) * NNN * 8, (e + uahead + 1) * NNN * 8,
+                             num_elements * NNN * 8);
     }
     const int K0 = h * KH, NK = h ? N - KH : KH;
 

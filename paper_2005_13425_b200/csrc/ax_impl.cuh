@@ -383,7 +383,9 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     const int64_t resident = (int64_t)sm_count() * MINB;
     const int64_t grid = PERSIST ? (nbatches < resident ? nbatches : resident) : nbatches;
     // prefetch distance: the batch that replaces this one on its SM
-    int64_t pf = L2PF == 2 ? 0 : ((nbatches > resident) ? resident * SLOTS : -1);
+    int64_t pf = L2PF == 2 ? 0
+               : L2PF == 3 ? ((nbatches > resident) ? resident * SLOTS : 0)
+                           : ((nbatches > resident) ? resident * SLOTS : -1);
     static const char* pf_env = getenv("SEM_AX_PFDIST");  // tuning probe
     if (pf_env) pf = atoll(pf_env);
     if (cgp.grid_out) *cgp.grid_out = (unsigned)grid;
@@ -427,7 +429,7 @@ static int try_pencil(const double* u, const double* g, const double* dx, double
 // Half-pencil kernel (ax_half.cuh): two threads per k-pencil, large n.
 template <int N, int MINB, int PD, bool FOLD>
 static int launch_half(const double* u, const double* g, const double* dx, double* w, int64_t E,
-                       cudaStream_t stream)
+                       cudaStream_t stream, bool uahead = false)
 {
     using C = HalfCfg<N>;
     if constexpr (C::THREADS > 1024 || C::SMEM * MINB > 227 * 1024) {
@@ -437,7 +439,7 @@ static int launch_half(const double* u, const double* g, const double* dx, doubl
         DParamP<N> D;
         const bool antisym = fill_dparam<N>(D, dx);
         if constexpr (FOLD) {
-            if (!antisym) return launch_half<N, MINB, PD, false>(u, g, dx, w, E, stream);
+            if (!antisym) return launch_half<N, MINB, PD, false>(u, g, dx, w, E, stream, uahead);
         }
         if (E == 0) return 0;
         if (E > 0x7fffffffLL) {
@@ -455,7 +457,9 @@ static int launch_half(const double* u, const double* g, const double* dx, doubl
             if (err != cudaSuccess) return fail_cuda(err, "sem_ax: cudaFuncSetAttribute");
             configured.fetch_or(bit, std::memory_order_release);
         }
-        kern<<<(unsigned)E, C::THREADS, C::SMEM, stream>>>(u, g, w, E, D);
+        const int64_t resident = (int64_t)sm_count() * MINB;
+        kern<<<(unsigned)E, C::THREADS, C::SMEM, stream>>>(u, g, w, E, D,
+                                                           uahead && E > resident ? resident : 0);
         SEM_CHECK_LAUNCH("sem_ax (half-pencil) launch");
         return 0;
     }
@@ -513,8 +517,11 @@ static int launch_split(const double* u, const double* g, const double* dx, doub
 // and 185 -> 182 us).
 // Round 2 (two full sweeps, tools/gpu_psweep.sh, profiles/r02_ax_psweep.txt):
 // n = 2 -> 10, 4 -> 17 (-21%: 3.9 vs 5.0 us), 7 -> 40, 8 -> 40, 9 -> 41
-// (1.6-3.1%, the same winner in both sweeps).
-constexpr int kDefaultVariant[17] = {0, 0, 10, 5, 17, 34, 38, 40, 40, 41, 34, 41, 57, 55, 59, 62, 61};
+// (1.6-3.1%, the same winner in both sweeps); n = 12 -> 75 (half-pencil
+// with the u block a resident wave ahead in L2: 73.2 vs 75.5 us), n = 13 ->
+// 74 (the same prefetch on the register-ring pencil: 97.3 vs 99.4 us),
+// confirmed by a second run (profiles/r02_ax_uahead.txt).
+constexpr int kDefaultVariant[17] = {0, 0, 10, 5, 17, 34, 38, 40, 40, 41, 34, 41, 75, 74, 59, 62, 61};
 
 template <int N>
 static int ax_n(const double* u, const double* g, const double* dx, double* w, int64_t E,
@@ -589,6 +596,13 @@ static int ax_n(const double* u, const double* g, const double* dx, double* w, i
         case 68: return launch_split<N, 6, 0, true, true>(u, g, dx, w, E, stream, pdl);
         case 69: return launch_split<N, 3, 0, true, true>(u, g, dx, w, E, stream, pdl);
         case 70: return launch_split<N, 8, 0, true, true>(u, g, dx, w, E, stream, pdl);
+        // large n: as 61 / 62 / 54 / 55 / 59 with the u block of the element
+        // a resident wave ahead also prefetched into L2 (L2PF 3)
+        case 71: return try_pencil<N, 1, 2, false, 2, 3, 0, true, 0, true>(u, g, dx, w, E, stream, pa);
+        case 72: return try_pencil<N, 1, 2, false, 3, 3, 0, true, 0, true>(u, g, dx, w, E, stream, pa);
+        case 73: return try_pencil<N, 1, 2, false, 3, 3, 0, true>(u, g, dx, w, E, stream, pa);
+        case 74: return try_pencil<N, 1, 2, false, 4, 3, 0, true>(u, g, dx, w, E, stream, pa);
+        case 75: return launch_half<N, 2, 1, true>(u, g, dx, w, E, stream, true);
         case 1: return launch_ax<N>(u, g, dx, w, E, stream);
         case 2: return try_pencil<N, S, 1, true>(u, g, dx, w, E, stream, pa);
         case 3: return try_pencil<N, (S + 1) / 2, 2, false>(u, g, dx, w, E, stream, pa);

@@ -514,7 +514,18 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         // (L2PF 1: the one that replaces it a resident wave later; L2PF 2:
         // pf_elems = 0, its own element -- the whole block is requested at
         // once, so the register-ring loads that follow hit L2)
-        if (L2PF && pf_elems >= 0 && lane_ok && p == 0 && e + pf_elems < num_elements) {
+        // (L2PF 3: its own element's u and g, and the u of the element a
+        // resident wave later -- that CTA's S3 u-column loads then hit L2
+        // instead of paying DRAM latency at its start; 27 KB per element at
+        // n = 15, so the wave-ahead data is ~8 MB, not the 64 MB a whole
+        // wave-ahead element costs in L2)
+        if (L2PF == 3 && lane_ok && p == 0 && active) {
+            prefetch_l2_bulk(u, e * NNN * 8, (e + 1) * NNN * 8, num_elements * NNN * 8);
+            prefetch_l2_bulk(g, e * 6 * NNN * 8, (e + 1) * 6 * NNN * 8, num_elements * 6 * NNN * 8);
+            if (pf_elems > 0 && e + pf_elems < num_elements)
+                prefetch_l2_bulk(u, (e + pf_elems) * NNN * 8, (e + pf_elems + 1) * NNN * 8,
+                                 num_elements * NNN * 8);
+        } else if (L2PF && pf_elems >= 0 && lane_ok && p == 0 && e + pf_elems < num_elements) {
             const int64_t en = e + pf_elems;
             prefetch_l2_bulk(u, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);
             if constexpr (CGM != 0) {
