@@ -9,6 +9,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -93,6 +94,9 @@ def main():
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--copy", action="store_true", help="also time a same-bytes copy")
     ap.add_argument("--repeat", type=int, default=1, help="timings per variant (best kept)")
+    ap.add_argument("--cool", type=float, default=0.0,
+                    help="seconds idle before each timing (back-to-back timings soak the "
+                         "1000 W power cap and bias a sweep toward the variants timed first)")
     args = ap.parse_args()
     hbm = float(measured_peaks(ROOT)["hbm_gbs"])
     lib = load()
@@ -114,7 +118,12 @@ def main():
                                basis.diff, basis.diff_t)
             for v in variants:
                 try:
-                    ms = min(time_variant(sets, basis, v, args.reps) for _ in range(args.repeat))
+                    ts = []
+                    for _ in range(args.repeat):
+                        if args.cool > 0:
+                            time.sleep(args.cool)
+                        ts.append(time_variant(sets, basis, v, args.reps))
+                    ms = min(ts)
                 except Exception as exc:  # noqa: BLE001
                     print(json.dumps({"n": n, "E": E, "variant": v, "error": str(exc)}))
                     continue
