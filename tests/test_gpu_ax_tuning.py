@@ -139,3 +139,20 @@ def test_ax_pdl_dependent_chain(cuda, E, v):
     ref1 = O.ax_layered(u0[idx].cpu().numpy(), g[idx].cpu().numpy(), b.diff, b.diff_t)
     assert O.rel_diff(w[idx].cpu().numpy(), ref1) <= AX_TOL
     assert float(np.abs(ref[1].cpu().numpy()).max()) > 0
+
+
+@pytest.mark.parametrize("n", [12, 13, 14, 15, 16])
+def test_ax_wave_ahead_u_tilings_e4096(cuda, n):
+    """Large-n tilings that also prefetch the u block of the element a
+    resident wave ahead into L2 (71-74 pencil, 75 half-pencil): engaged only
+    when E exceeds one resident wave, so checked at E = 4096."""
+    E = 4096
+    u, g = _inputs(E, n, 900 + n, 950 + n)
+    b = sb.build_basis(n)
+    idx = sorted({0, 1, 295, 296, 297, E // 2, E - 2, E - 1})
+    for v in (71, 72, 73, 74, 75):
+        w = torch.full_like(u, float("nan"))
+        apply_ax_into(u, g, b, w, v)
+        torch.cuda.synchronize()
+        assert not torch.isnan(w).any(), f"variant {v}: unwritten output"
+        assert _check(u, g, w, b, idx) <= AX_TOL, f"variant {v}"

@@ -28,6 +28,16 @@ for n in (3, 4, 6, 7, 8, 10, 11, 12, 14, 16):
     sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(4, 0.0))
     sb.cg_solve(f, lambda x: sb.apply_global(x, geom, b, topo), topo, sb.CgConfig(3, 0.0))
     sb.weighted_dot(f, f, topo)
+# large-n tilings with the wave-ahead u prefetch need more elements than one
+# resident wave (E > 2 x 148) to engage it
+for n in (12, 13):
+    E = 320
+    b = sb.build_basis(n)
+    u = sb.random_field(E, n, 3, device=dev)
+    gv = sb.random_field(6 * E, n, 4, device=dev).reshape(E, 6, n, n, n)
+    w = torch.empty_like(u)
+    for var in (0, 71, 72, 73, 74, 75):
+        apply_ax_into(u, gv, b, w, var)
 import warnings  # noqa: E402
 with warnings.catch_warnings():
     warnings.simplefilter("ignore")
