@@ -794,9 +794,12 @@ def bench_cg(sb, dev, iters):
     model_flops = perf.model_flops_per_iteration(dofs, n)
     hbm = float(perf.measured_peaks(ROOT)["hbm_gbs"]) * 1e9
     gf = model_flops / (per_it * 1e-3)
+    design_bytes = 120 * E * n ** 3  # the fused design's algorithmic traffic
     return {"iterations": res.iterations_run, "ms_per_iteration": per_it,
             "model_gflops": gf / 1e9,
             "paper_roofline_frac": gf / perf.roofline_peak(hbm, n),
+            "design_bytes_per_iteration": design_bytes,
+            "design_roofline_frac": design_bytes / (per_it * 1e-3) / hbm,
             "final_residual": float(res.residual_history[-1]),
             "note": "paper Eq.(1)/(2) model: D(12n+34) flop, 240 D bytes per iteration; "
                     "timed with CUDA events incl. one host sync at the end"}
@@ -898,6 +901,8 @@ def bench_cg_weak(sb, dev, world, rank, iters, force_slab=False):
     out = {"global_box": [ex, ey, ez], "elements_per_gpu": per, "iterations": iters,
            "ms_per_iteration": per_it, "model_gflops_total": model / 1e9,
            "model_gflops_per_gpu": model / 1e9 / world, "final_residual": hist_last,
+           "design_roofline_frac_per_gpu": 120 * per * n ** 3 / (per_it * 1e-3)
+           / (float(perf.measured_peaks(ROOT)["hbm_gbs"]) * 1e9),
            "path": path, "timing": "CUDA events, max over ranks"}
     if not (world == 1 and not force_slab):
         out["phases_us_per_iteration_by_rank"] = every
