@@ -623,7 +623,7 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
-def _graph_us(dev, launch, count, total):
+def _graph_us(dev, launch, count, total, cool=0.0):
     """Device microseconds per launch: `count` launches (launch(i) enqueues
     the i-th on the current stream) captured in one CUDA graph, a warm burst
     of replays, then ceil(total / count) replays timed with CUDA events --
@@ -643,6 +643,8 @@ def _graph_us(dev, launch, count, total):
     stream = torch.cuda.current_stream(dev)
     best = None
     for _ in range(2):
+        if cool > 0:  # idle first: each window starts below the power cap
+            time.sleep(cool)
         for _ in range(max(1, reps // 2)):  # warm burst
             graph.replay()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -670,7 +672,7 @@ def _ax_sets(sb, dev, E, n, seed):
     return sets
 
 
-def _copy_us(dev, nbytes, nsets, count, total):
+def _copy_us(dev, nbytes, nsets, count, total, cool=0.0):
     """Same-bytes reference: sem_stream_copy moving nbytes per launch (half
     read, half written), rotating over nsets buffer pairs, same protocol."""
     import torch
@@ -685,7 +687,7 @@ def _copy_us(dev, nbytes, nsets, count, total):
         rc = lib.sem_stream_copy(dst.data_ptr(), src.data_ptr(), half,
                                  torch.cuda.current_stream(dev).cuda_stream)
         assert rc == 0, "sem_stream_copy"
-    us = _graph_us(dev, launch, count, total)
+    us = _graph_us(dev, launch, count, total, cool)
     del bufs
     return us
 
@@ -717,7 +719,7 @@ def bench_ax_sizes(sb, dev, basis, stream, steps=600):
     return out
 
 
-def bench_psweep(sb, dev, steps=300):
+def bench_psweep(sb, dev, window_us=15000.0):
     """BASELINE config 3: the tuned default Ax for every n = 2..16 at
     E = 4096, same protocol, with the same-bytes copy beside each n (for
     n <= 6 the rotation fits in L2 and a ~2-10 us launch is ramp-bound: the
@@ -733,9 +735,14 @@ def bench_psweep(sb, dev, steps=300):
         sets = _ax_sets(sb, dev, E, n, 700)
         nsets = len(sets)
         count = nsets * max(1, 30 // nsets)
+        # ~15 ms windows after an idle gap: the burst regime the headline and
+        # MEASURED_PEAKS are taken in (longer back-to-back windows at n >= 12
+        # run into the 1000 W cap and drift 3-5% slower)
+        est_us = ax_bytes(E, n) / 6.0e3  # bytes / (6 GB/ms) ~ us per apply
+        steps = max(count, min(3000, int(window_us / est_us)))
         us = _graph_us(dev, lambda i: apply_ax_into(*sets[i % nsets][:2], basis, sets[i % nsets][2]),
-                       count, steps)
-        cus = _copy_us(dev, ax_bytes(E, n), nsets, count, steps)
+                       count, steps, cool=0.2)
+        cus = _copy_us(dev, ax_bytes(E, n), nsets, count, steps, cool=0.2)
         out[str(n)] = {"us_per_apply": round(us, 3), "gflops": round(ax_flops(E, n) / us / 1e3, 1),
                        "hbm_frac": round(ax_bytes(E, n) / (us * 1e3) / hbm, 4),
                        "same_bytes_copy_us": round(cus, 3),
