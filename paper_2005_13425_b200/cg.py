@@ -35,9 +35,14 @@ __all__ = ["CgConfig", "CgResult", "CgBreakdownError", "weighted_dot", "cg_solve
 
 CG_VECTOR_FLOPS_PER_POINT = 12
 USE_GRAPHS = True  # replay captured iterations (fused path)
-# iterations per captured graph: 1 measured best (tools/cg_graph_k.py: 5-20
-# iterations per graph ran 3-8% slower per iteration at E = 4096 and 32768)
-GRAPH_ITERATIONS = 1
+# iterations per captured graph: 10.  Inside one graph the next iteration's
+# Ax is a programmatic dependent of the previous update (csrc/cg.cu cg_pdl),
+# so its CTAs start loading the metric while the update drains; between graph
+# launches that overlap is lost.  tools/cg_ab.py with idle gaps between
+# configurations (profiles/r02_cg_graph_pdl.txt): E = 4096 98.0-99.2 us per
+# iteration at 1 -> 93.8-94.9 us at 10; round 1's "1 is best" came from
+# back-to-back solves whose power-cap drift hid the difference.
+GRAPH_ITERATIONS = 10
 # graph replays between non-blocking polls of the device stop flag
 POLL_EVERY = 8
 _STOP_OFFSET = sem_cg_state.stop.offset
@@ -222,10 +227,10 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
         finalize()
         st = ws.read_state()
     elif callback is None:
-        if cfg.max_iterations > 2 and USE_GRAPHS:
-            # iteration 1 launched directly (configures the kernels), then one
-            # iteration is captured into a CUDA graph and replayed: the
-            # iteration's launches are parameter-stable (scalars live in the
+        if cfg.max_iterations > max(2, GRAPH_ITERATIONS) and USE_GRAPHS:
+            # iteration 1 launched directly (configures the kernels), then
+            # GRAPH_ITERATIONS iterations are captured into one CUDA graph and
+            # replayed: the launches are parameter-stable (scalars live in the
             # device state), so replay == relaunch without the host overhead.
             # Early exits are device-side (queued launches become no-ops); the
             # host also polls the stop flag without blocking (an async copy
@@ -233,7 +238,9 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
             # has completed) and stops replaying once the solve has ended.
             run(1)
             rest = cfg.max_iterations - 1
-            k = max(1, min(GRAPH_ITERATIONS, rest))
+            # always the same graph size (a short solve runs its iterations
+            # directly instead of capturing -- and evicting -- another graph)
+            k = max(1, GRAPH_ITERATIONS)
             key = (g.data_ptr(), box, dx.tobytes(), k)
             graph = ws.iteration_graph(lambda: run(k), key)
             stream = torch.cuda.current_stream(dev)
@@ -241,7 +248,7 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
             ws._stop_event = None
             for q in range(rest // k):
                 graph.replay()
-                if (q + 1) % POLL_EVERY == 0:
+                if (q + 1) % max(1, POLL_EVERY // k) == 0:
                     if ws._stop_event is not None and ws._stop_event.query() \
                             and int(ws._stop_host[0]) != 0:
                         break

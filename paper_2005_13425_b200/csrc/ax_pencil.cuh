@@ -321,6 +321,9 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
 
     double beta = 0.0, alpha_prev = 0.0, pap_s = 1.0;
     bool xpend = false;
+#ifdef SEM_TRACE
+    unsigned long long _sem_t0 = sem_gtimer(), _sem_t1 = 0;
+#endif
     // GMODE 4: every bulk copy of the CTA (p, r, x, g) is issued before the
     // CG scalars are read, so the state round trip overlaps the transfers;
     // x is staged unconditionally (unused on the first iteration)
@@ -337,6 +340,9 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             bulk_g2s(Gbase, g + batch * (6 * NNN), 6 * NNN * 8, gbar);
         }
         griddep_wait();
+#ifdef SEM_TRACE
+        _sem_t1 = sem_gtimer();
+#endif
         if (tid == 0) {
             const int64_t e0 = batch;
             mbar_expect_tx(ubar, (unsigned)(3 * NNN * 8));
@@ -678,6 +684,15 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
         __shared__ bool red_last;
         griddep_launch();  // late trigger: the dependent launches as this grid drains
         const double tot = block_sum<THREADS>(pap_acc, red_sh);
+#ifdef SEM_TRACE
+        if (CGM == 2 && tid == 0) {
+            unsigned long long* _tr = reinterpret_cast<unsigned long long*>(cgp.st + 1) +
+                                      (0 * 128 + (cgp.st->it & 127)) * 3;
+            atomicMin(_tr, _sem_t0);
+            atomicMin(_tr + 1, _sem_t1);
+            atomicMax(_tr + 2, sem_gtimer());
+        }
+#endif
         if (cgp.deferred) {
             // the CTA retires at once: a per-CTA fence + atomic would hold
             // its shared memory for a full memory round trip

@@ -290,7 +290,9 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
                   int nranks = 0)
 {
     constexpr int NN = N * N, NNN = N * N * N;
+    SEM_TRACE_ENTRY(st);
     griddep_wait();
+    SEM_TRACE_WAITED(st);
     if (st->stop) return;
     double alpha;
     if (DIST && gathered != nullptr) {
@@ -335,6 +337,7 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         }
         store_row<N>(r + base, rv);
     }
+    if (!DIST) SEM_TRACE_EXIT(st, 2);
     griddep_launch();
     const double vals[1] = {acc};
     if (deferred) {  // single GPU: cg_settle_kernel finishes <r, r>
@@ -594,10 +597,13 @@ __global__ void __launch_bounds__(kSettleThreads)
 cg_settle_kernel(const double* __restrict__ partials, int count, sem_cg_state* st,
                  double* history, int accumulate = 0)
 {
+    SEM_TRACE_ENTRY(st);
     griddep_wait();
+    SEM_TRACE_WAITED(st);
     griddep_launch();
     if (st->stop) return;
     const double tot = settle_sum<kSettleThreads>(partials, count);
+    SEM_TRACE_EXIT(st, 1);
     if (threadIdx.x != 0) return;
     if (PH == kPhaseLocal) st->local_sum = (accumulate ? st->local_sum : 0.0) + tot;
     else fin_phase(st, PH, tot, history);
@@ -619,12 +625,18 @@ static int fin_mode()
     return k;
 }
 // programmatic dependent launch of the iteration chain (SEM_CG_PDL: 0 off,
-// 1 every launch, 2 (default) the settle and update launches only: they are
-// small / register-only, so launching them while the Ax grid drains costs it
-// no residency; tools/cg_tune7.sh: E = 4096 96.3 -> 95.0 us per iteration)
+// 1 (default) every launch, 2 the settle and update launches only).  With
+// several iterations captured per CUDA graph (cg.py GRAPH_ITERATIONS) the
+// next iteration's Ax CTAs become resident as the update drains and issue
+// their metric bulk copy before griddep_wait; a timeline trace (-DSEM_TRACE,
+// tools/cg_trace.py) showed ~5-7 us between the update's end and the next
+// Ax's first CTA when every iteration was its own graph launch.  Measured
+// with idle gaps (tools/cg_ab.py, profiles/r02_cg_graph_pdl.txt): E = 4096
+// 98.0-99.2 us (1 iteration per graph) -> 93.8-94.9 us (10 per graph, PDL
+// on every launch); E = 32768 619-622 -> 605-614 us.
 static int cg_pdl()
 {
-    static const int k = getenv("SEM_CG_PDL") ? atoi(getenv("SEM_CG_PDL")) : 2;
+    static const int k = getenv("SEM_CG_PDL") ? atoi(getenv("SEM_CG_PDL")) : 1;
     return k;
 }
 

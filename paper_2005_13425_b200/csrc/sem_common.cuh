@@ -50,6 +50,36 @@ __device__ __forceinline__ void griddep_launch()
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Timeline tracing of the fused CG chain (diagnostic builds only,
+// -DSEM_TRACE; tools/cg_trace.py): per kernel kind and iteration slot, the
+// earliest CTA entry, the earliest return from griddep_wait and the latest
+// CTA exit (%globaltimer ns), kept in a caller-provided area right after
+// the sem_cg_state struct.  Compiled out of the product build.
+#ifdef SEM_TRACE
+__device__ __forceinline__ unsigned long long sem_gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SEM_TRACE_ENTRY(st) const unsigned long long _sem_t0 = sem_gtimer();
+#define SEM_TRACE_WAITED(st) const unsigned long long _sem_t1 = sem_gtimer();
+#define SEM_TRACE_EXIT(st, kid)                                                             \
+    do {                                                                                    \
+        if (threadIdx.x == 0) {                                                             \
+            unsigned long long* _tr = reinterpret_cast<unsigned long long*>((st) + 1) +      \
+                                      ((kid) * 128 + ((st)->it & 127)) * 3;                  \
+            atomicMin(_tr, _sem_t0);                                                        \
+            atomicMin(_tr + 1, _sem_t1);                                                    \
+            atomicMax(_tr + 2, sem_gtimer());                                               \
+        }                                                                                   \
+    } while (0)
+#else
+#define SEM_TRACE_ENTRY(st)
+#define SEM_TRACE_WAITED(st)
+#define SEM_TRACE_EXIT(st, kid)
+#endif
+
 // Launch `kern` on `stream`, with programmatic stream serialization when
 // `pdl` is set (the kernel must call griddep_wait() before touching anything
 // its predecessors write).

@@ -367,8 +367,9 @@ def test_cg_fused_vs_golden(cuda, golden, key):
 
 
 def test_cg_graph_replay_matches_eager(cuda):
-    """The fused solver replays one captured CUDA-graph iteration; it must
-    equal eager launching bit for bit."""
+    """The fused solver replays captured CUDA graphs of GRAPH_ITERATIONS
+    iterations (programmatic dependent launches inside); it must equal eager
+    launching bit for bit, including a remainder run directly."""
     from paper_2005_13425_b200 import cg as C
     b, topo, geom, f = _cg_problem(2, 2, 2, 6)
     op = sb.GlobalOperator(geom, b, topo)

@@ -12,7 +12,8 @@ from paper_2005_13425_b200 import cg as C  # noqa: E402
 
 dev = torch.device("cuda", 0)
 out = {}
-for k in (1, 5, 10, 20, 1, 10):
+KS = [int(x) for x in os.environ.get("CG_GRAPH_KS", "1,5,10,20,1,10").split(",")]
+for k in KS:
     C.GRAPH_ITERATIONS = k
     row = {}
     for E in (4096, 32768):

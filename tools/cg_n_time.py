@@ -19,7 +19,7 @@ for n in [int(a) for a in (sys.argv[1:] or ["4", "6", "8", "10", "12"])]:
     f = sb.make_rhs(E, n, topo, sb.mix64(1, E), device=dev)
     op = sb.GlobalOperator(geom, b, topo)
     ws = sb.CgWorkspace(topo, 50, dev)
-    sb.cg_solve(f, op, topo, sb.CgConfig(3, 0.0), workspace=ws)
+    sb.cg_solve(f, op, topo, sb.CgConfig(50, 0.0), workspace=ws)  # warm-up (captures)
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
