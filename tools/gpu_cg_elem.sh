@@ -1,2 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for env in "SEM_CG_AX_CFG=0" "SEM_CG_AX_CFG=11" "SEM_CG_AX_CFG=12" "SEM_CG_AX_CFG=9" "SEM_CG_AX_CFG=0"; do echo "$env $(env $env timeout 300 python tools/cg_time.py 4096 32768 2>&1 | tail -1)"; done > gpurun_out/cg_elem.txt
+timeout 600 python -m pytest tests/test_gpu_cg_modes.py -q -x > gpurun_out/cg_modes.log 2>&1
+for env in "SEM_CG_UPD_EARLY=0" "SEM_CG_UPD_EARLY=1"; do env $env CG_REPS=3 CG_GRAPH_KS=10 python tools/cg_ab.py; done > gpurun_out/cg_early.txt 2>&1
+for env in "SEM_CG_UPD_EARLY=0" "SEM_CG_UPD_EARLY=1"; do env $env CG_E=32768 CG_REPS=2 CG_GRAPH_KS=10 python tools/cg_ab.py; done >> gpurun_out/cg_early.txt 2>&1
