@@ -43,16 +43,24 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def _compile_flags(verbose: bool = False) -> list:
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    # tuning experiments: extra -D definitions (e.g. SEM_NVCC_DEFS="SEM_UPD_MINB=8")
+    flags += [f"-D{d}" for d in os.environ.get("SEM_NVCC_DEFS", "").split()]
+    if verbose:
+        flags += ["-Xptxas", "-v"]
+    return flags
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile every translation unit concurrently (one nvcc per .cu), then
-    link the shared library."""
-    if not force and not _stale():
+    link the shared library.  Rebuilt when a source is newer than the library
+    or the -D set (SEM_NVCC_DEFS) differs from the one it was built with."""
+    compile_flags = _compile_flags(verbose)
+    flag_file = OUT + ".flags"
+    built_with = open(flag_file).read() if os.path.exists(flag_file) else None
+    if not force and not _stale() and built_with == " ".join(compile_flags):
         return OUT
-    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
-    # tuning experiments: extra -D definitions (e.g. SEM_NVCC_DEFS="SEM_UPD_MINB=8")
-    compile_flags += [f"-D{d}" for d in os.environ.get("SEM_NVCC_DEFS", "").split()]
-    if verbose:
-        compile_flags += ["-Xptxas", "-v"]
     # objects are cached per flag set outside the tree (SEM_OBJ_CACHE): a unit
     # is recompiled when its .cu, any header or the flags changed
     cache = os.environ.get("SEM_OBJ_CACHE")
@@ -87,6 +95,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             "-o", OUT + ".tmp", *objs]
     subprocess.run(link, check=True)
     os.replace(OUT + ".tmp", OUT)
+    with open(flag_file, "w") as fh:
+        fh.write(" ".join(compile_flags))
     if not (cache and not force):
         shutil.rmtree(objdir, ignore_errors=True)
     return OUT

@@ -41,6 +41,8 @@ torch.cuda.synchronize()
 res = sb.cg_solve(f, op, topo, sb.CgConfig(iters, 0.0), workspace=ws)
 torch.cuda.synchronize()
 t = tr.cpu().numpy().astype(np.float64)
+print("nonzero exits per kernel:", [(int((t[k, :, 2] > 0).sum())) for k in range(3)], "iterations", res.iterations_run,
+      file=sys.stderr)
 rows = []
 for it in range(10, 90):
     k0 = t[0, it, 0]
