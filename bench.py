@@ -794,13 +794,16 @@ def bench_cg(sb, dev, iters):
     from paper_2005_13425_b200 import cg as C
     sb.cg_solve(f, op, topo, sb.CgConfig(C.GRAPH_ITERATIONS + 2, 0.0), workspace=ws)
     torch.cuda.synchronize(dev)
-    time.sleep(0.5)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    res = sb.cg_solve(f, op, topo, sb.CgConfig(iters, 0.0), workspace=ws)
-    e1.record()
-    torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1)
+    solves = []
+    for _ in range(3):  # median of 3 solves, each after a short idle gap
+        time.sleep(0.3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = sb.cg_solve(f, op, topo, sb.CgConfig(iters, 0.0), workspace=ws)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        solves.append(e0.elapsed_time(e1))
+    ms = statistics.median(solves)
     dofs = topo.dofs
     per_it = ms / iters
     model_flops = perf.model_flops_per_iteration(dofs, n)
@@ -808,14 +811,15 @@ def bench_cg(sb, dev, iters):
     gf = model_flops / (per_it * 1e-3)
     design_bytes = 120 * E * n ** 3  # the fused design's algorithmic traffic
     return {"iterations": res.iterations_run, "ms_per_iteration": per_it,
+            "ms_per_iteration_solves": [x / iters for x in solves],
             "model_gflops": gf / 1e9,
             "paper_roofline_frac": gf / perf.roofline_peak(hbm, n),
             "design_bytes_per_iteration": design_bytes,
             "design_roofline_frac": design_bytes / (per_it * 1e-3) / hbm,
             "final_residual": float(res.residual_history[-1]),
             "note": "paper Eq.(1)/(2) model: D(12n+34) flop, 240 D bytes per iteration; "
-                    "timed with CUDA events incl. one host sync at the end, after a "
-                    "graph-capturing warm-up and 0.5 s idle"}
+                    "timed with CUDA events incl. one host sync at the end, median of 3 "
+                    "solves after a graph-capturing warm-up, 0.3 s idle before each"}
 
 
 NCCL_LOG = "/tmp/sem_bench_nccl_rankRANK.log"
