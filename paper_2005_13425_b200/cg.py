@@ -109,12 +109,16 @@ class CgWorkspace:
         # one allocation, [x | p | r | w | w2]: the vectors an iteration
         # re-reads soonest (r, w; then p) are adjacent, so one L2 access-policy
         # window can cover them (_l2_window)
+        # (each vector starts on a 16-byte boundary: the kernels move even-n
+        # rows as 128-bit accesses and the settle reads the partials so)
         m = topo.num_elements * topo.n ** 3
-        self._buf = torch.empty(5 * m, dtype=torch.float64, device=device)
-        v = [self._buf[q * m:(q + 1) * m].view(shape) for q in range(3)]
+        mp = m + (m & 1)
+        self._buf = torch.empty(3 * mp + 2 * m, dtype=torch.float64, device=device)
+        v = [self._buf[q * mp:q * mp + m].view(shape) for q in range(3)]
         self.x, self.p, self.r = v
-        self.w = self._buf[3 * m:].view((2,) + shape)
+        self.w = self._buf[3 * mp:].view((2,) + shape)
         self._m = m
+        self._mp = mp
         self.history = torch.zeros(max(1, max_iterations), dtype=torch.float64, device=device)
         self.state = torch.zeros(ctypes_sizeof_state(), dtype=torch.uint8, device=device)
         self.scratch = torch.zeros(int(load().sem_reduce_scratch_bytes()), dtype=torch.uint8,
@@ -161,7 +165,7 @@ def _l2_window(ws: CgWorkspace, stream) -> bool:
     mode = os.environ.get("SEM_CG_L2", "off")
     if mode == "off":
         return False
-    m8 = ws._m * 8
+    m8 = ws._mp * 8
     first = {"rw": 2, "prw": 1, "xprw": 0}[mode]
     base = ws._buf.data_ptr() + first * m8
     nbytes = (4 - first) * m8

@@ -853,9 +853,12 @@ extern "C" int sem_cg_run(const double* g, const double* dx, const double* dxt, 
     const int64_t E = (int64_t)ex * ey * ez;
     const int64_t m = E * n * n * n;
     auto* rs = static_cast<ReduceScratch*>(scratch);
-    // w holds two E*n^3 vectors: local Ax output, then the assembled field
+    // w holds two E*n^3 vectors: the local Ax output, then the per-CTA
+    // partial slots -- started on an even double so the settle's 16-byte
+    // loads are aligned when E*n^3 is odd (odd E and odd n; the slots need
+    // at most E < E*n^3 - 1 doubles, so the shift stays inside w)
     double* w_local = w;
-    double* w_asm = w + m;
+    double* w_asm = w + m + (m & 1);
     SEM_SWITCH_N(n, return cg_run_n<NV>(g, dx, x, r, p, w_local, w_asm, state, history,
                                         iterations, E, bx, rs, s));
 }
@@ -911,8 +914,8 @@ extern "C" int sem_cg_run_phases(const double* g, const double* dx, const double
         rc = fail_cuda(err, "sem_cg_run_phases: events");
     }
     if (rc == 0) {
-        SEM_SWITCH_N(n, rc = cg_run_n<NV>(g, dx, x, r, p, w, w + m, state, history, iterations, E,
-                                          bx, rs, s, marks); break);
+        SEM_SWITCH_N(n, rc = cg_run_n<NV>(g, dx, x, r, p, w, w + m + (m & 1), state, history,
+                                          iterations, E, bx, rs, s, marks); break);
     }
     if (rc == 0 && (err = cudaEventSynchronize(marks[nev - 1])) != cudaSuccess)
         rc = fail_cuda(err, "sem_cg_run_phases: sync");

@@ -366,6 +366,20 @@ def test_cg_fused_vs_golden(cuda, golden, key):
     assert int(np.sum(bar == CG_TOL)) >= iters - 5
 
 
+@pytest.mark.parametrize("box,n", [((3, 3, 3), 7), ((5, 3, 1), 5)])
+def test_cg_fused_odd_point_count(cuda, box, n):
+    """E n^3 odd (odd E and odd n): the per-CTA partial slots after the local
+    Ax output must still start 16-byte aligned (found by the C client)."""
+    ex, ey, ez = box
+    b, topo, geom, f = _cg_problem(ex, ey, ez, n)
+    assert (ex * ey * ez * n ** 3) % 2 == 1
+    res = sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(25, 0.0))
+    T = O.BoxTopology(ex, ey, ez, n)
+    g = O.box_geom(ex, ey, ez, b.weights, 1.0)
+    _, hist, _ = O.cg(_np(f), lambda p: O.apply_global(p, g, b.diff, b.diff_t, T), T, 25)
+    assert _rel_hist(res.residual_history, hist) <= CG_TOL
+
+
 def test_cg_graph_replay_matches_eager(cuda):
     """The fused solver replays captured CUDA graphs of GRAPH_ITERATIONS
     iterations (programmatic dependent launches inside); it must equal eager
