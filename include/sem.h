@@ -10,6 +10,11 @@
  * stream) without synchronising the host.  Every entry point returns 0 on
  * success, otherwise a nonzero code with a message in sem_last_error().
  * No entry point allocates device memory; scratch is caller-provided.
+ * Alignment: the metric g must be 16-byte aligned (it moves by bulk copies);
+ * fields (u, w, f, x, r, p) must be 16-byte aligned for even n and 8-byte
+ * aligned for odd n -- allocation bases always are, and since n^3 is even for
+ * even n, element sub-ranges keep the property.  Violations return
+ * SEM_E_INVALID before anything is enqueued.
  *
  * Reference interface each entry point replaces (the reference is the
  * Python/numba package `sembench`, paths relative to

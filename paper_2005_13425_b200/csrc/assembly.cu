@@ -146,6 +146,7 @@ extern "C" int sem_dssum_box(const double* f, double* out, int32_t ex, int32_t e
         sem::set_error("sem_dssum_box: null pointer or in-place call (out must differ from f)");
         return SEM_E_INVALID;
     }
+    if (int rc = sem::check_fields_aligned("sem_dssum_box", n, nullptr, {f, out})) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (int rc = sem::bind_stream_device(s)) return rc;
     return sem::dssum_box(f, out, ex, ey, ez, n, apply_mask != 0, s);
@@ -159,6 +160,7 @@ extern "C" int sem_mask_box(const double* f, double* out, int32_t ex, int32_t ey
         sem::set_error("sem_mask_box: null pointer");
         return SEM_E_INVALID;
     }
+    if (int rc = sem::check_fields_aligned("sem_mask_box", n, nullptr, {f, out})) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (int rc = sem::bind_stream_device(s)) return rc;
     return sem::mask_box(f, out, ex, ey, ez, n, s);

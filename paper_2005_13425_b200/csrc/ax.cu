@@ -78,6 +78,7 @@ extern "C" int sem_ax_variant(const double* u, const double* g, const double* dx
         sem::set_error("sem_ax: null pointer or negative element count");
         return SEM_E_INVALID;
     }
+    if (int rc = sem::check_fields_aligned("sem_ax", n, g, {u, w})) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (int rc = sem::bind_stream_device(s)) return rc;
     return sem::ax_dispatch(u, g, dx, w, num_elements, n, variant, s, -1);

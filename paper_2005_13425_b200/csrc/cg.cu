@@ -827,6 +827,7 @@ extern "C" int sem_cg_init(const double* f, double* x, double* r, double* p, sem
         set_error("sem_cg_init: bad arguments");
         return SEM_E_INVALID;
     }
+    if (int rc = check_fields_aligned("sem_cg_init", n, nullptr, {f, x, r, p})) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (int rc = bind_stream_device(s)) return rc;
     const Box bx{ex, ey, ez, 0, ez};
@@ -847,6 +848,7 @@ extern "C" int sem_cg_run(const double* g, const double* dx, const double* dxt, 
         set_error("sem_cg_run: bad arguments");
         return SEM_E_INVALID;
     }
+    if (int rc = check_fields_aligned("sem_cg_run", n, g, {x, r, p, w})) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (int rc = bind_stream_device(s)) return rc;
     const Box bx{ex, ey, ez, 0, ez};

@@ -1,5 +1,7 @@
 // Shared helpers for libsem (B200 / sm_100a).
 #pragma once
+#include <cstdint>
+#include <initializer_list>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -79,6 +81,31 @@ __device__ __forceinline__ unsigned long long sem_gtimer()
 #define SEM_TRACE_WAITED(st)
 #define SEM_TRACE_EXIT(st, kid)
 #endif
+
+// Field-pointer alignment contract (checked before anything is enqueued, so
+// a bad pointer is an error code, not a device fault that poisons the
+// context): metric blocks move by bulk (TMA) copies -> 16 bytes; fields of an
+// even n are moved as 16-byte row pairs / bulk layers -> 16 bytes (n^3 is
+// even, so any element offset keeps it); odd n -> 8 bytes.
+inline bool aligned_to(const void* p, unsigned bytes)
+{
+    return (reinterpret_cast<uintptr_t>(p) & (uintptr_t)(bytes - 1)) == 0;
+}
+inline int check_fields_aligned(const char* who, int n, const void* metric,
+                                std::initializer_list<const void*> fields)
+{
+    if (metric && !aligned_to(metric, 16)) {
+        set_error("%s: the metric must be 16-byte aligned", who);
+        return SEM_E_INVALID;
+    }
+    const unsigned need = (n % 2 == 0) ? 16u : 8u;
+    for (const void* f : fields)
+        if (f && !aligned_to(f, need)) {
+            set_error("%s: field pointers must be %u-byte aligned for n = %d", who, need, n);
+            return SEM_E_INVALID;
+        }
+    return 0;
+}
 
 // Launch `kern` on `stream`, with programmatic stream serialization when
 // `pdl` is set (the kernel must call griddep_wait() before touching anything

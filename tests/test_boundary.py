@@ -75,3 +75,18 @@ def test_so_has_sm100a_code(lib):
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def test_alignment_contract_rejected_before_any_launch():
+    """Misaligned metric / field pointers are argument errors, reported before
+    any CUDA call (so this runs without a GPU) instead of device faults."""
+    from paper_2005_13425_b200._lib import load
+    lib = load()
+    dx = (ctypes.c_double * 100)()
+    base = 1 << 20  # never dereferenced: the check precedes every launch
+    rc = lib.sem_ax(base, base + 8, dx, dx, base + 4096, 4, 10, None)
+    assert rc == 1001 and b"16-byte" in lib.sem_last_error()
+    rc = lib.sem_ax(base + 8, base, dx, dx, base + 4096, 4, 10, None)
+    assert rc == 1001 and b"field pointers" in lib.sem_last_error()
+    rc = lib.sem_dssum_box(base + 8, base + 4096, 2, 2, 2, 4, 1, None)
+    assert rc == 1001
