@@ -137,6 +137,42 @@ int main(int argc, char** argv)
         fprintf(stderr, "write failed\n");
         return 5;
     }
+
+    /* host buffers, the reference's call shape: pageable (malloc) arrays go
+     * through the chunked copy-engine pipeline, mapped page-locked arrays
+     * through the one-launch zero-copy kernel */
+    double* uh = (double*)malloc(m * sizeof(double));
+    double* wh = (double*)malloc(m * sizeof(double));
+    double *up, *wp;
+    CU(cudaHostAlloc((void**)&up, m * sizeof(double), cudaHostAllocMapped));
+    CU(cudaHostAlloc((void**)&wp, m * sizeof(double), cudaHostAllocMapped));
+    CU(cudaMemcpy(uh, u, m * sizeof(double), cudaMemcpyDeviceToHost));
+    memcpy(up, uh, m * sizeof(double));
+    CK(sem_ax_host(uh, g, dx, dxt, wh, E, n, d, wcg, 2, s));  /* 2-element chunks */
+    CK(sem_ax_host(up, g, dx, dxt, wp, E, n, d, wcg, 0, s));
+    CU(cudaStreamSynchronize(s));
+    /* weighted dot and the unfused vector updates */
+    double* dot;
+    CU(cudaMalloc((void**)&dot, sizeof(double)));
+    CK(sem_glsc3_box(u, w, ex, ey, ez, n, dot, scratch, s));
+    CK(sem_add2s1(w, u, 0.75, m, s));   /* w = 0.75 w + u */
+    CK(sem_add2s2(u, g, -1.25, m, s));  /* u += -1.25 g[:m] */
+    CU(cudaStreamSynchronize(s));
+    char p2[1024];
+    FILE* fo;
+    snprintf(p2, sizeof p2, "%s/w_host.bin", dir);
+    if (!(fo = fopen(p2, "wb"))) return 5;
+    fwrite(wh, sizeof(double), m, fo);
+    fclose(fo);
+    snprintf(p2, sizeof p2, "%s/w_mapped.bin", dir);
+    if (!(fo = fopen(p2, "wb"))) return 5;
+    fwrite(wp, sizeof(double), m, fo);
+    fclose(fo);
+    if (write_dev(dir, "dot.bin", dot, 1) || write_dev(dir, "add2s1.bin", w, m) ||
+        write_dev(dir, "add2s2.bin", u, m)) {
+        fprintf(stderr, "write failed\n");
+        return 5;
+    }
     printf("sem_client ok: E=%lld n=%d iterations=%d\n", (long long)E, n, st.iterations_run);
     return 0;
 }

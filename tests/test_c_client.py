@@ -60,3 +60,18 @@ def test_c_client_matches_oracle(cuda, client, tmp_path, box, n, iters):
     assert got.shape == (iters,)
     assert float(np.max(np.abs(got - hist) / np.abs(hist))) <= 1e-10
     assert O.rel_diff(load("x.bin").reshape(shape), x_ref) <= 1e-10
+    # host buffers: pageable (chunked copy engines) and mapped (zero-copy)
+    w_dev = load("w.bin")
+    assert np.array_equal(load("w_host.bin"), w_dev)
+    assert O.rel_diff(load("w_mapped.bin"), w_dev) <= 1e-12
+    # weighted dot (deterministic tree: rounding-level vs the oracle) and the
+    # unfused vector updates (bit-exact: multiply rounded, then add)
+    wv = w_dev.reshape(shape)
+    dot_ref = O.wdot3(u, wv, T.inv_multiplicity)
+    assert abs(float(load("dot.bin")[0]) - dot_ref) <= 1e-13 * max(1.0, abs(dot_ref))
+    p1 = w_dev.copy()
+    O.scale_add(p1, u.reshape(-1), 0.75)              # p = 0.75 p + z
+    assert np.array_equal(load("add2s1.bin"), p1)
+    x1 = u.reshape(-1).copy()
+    O.axpy_into(x1, g.reshape(-1)[:u.size], -1.25)    # x += -1.25 y
+    assert np.array_equal(load("add2s2.bin"), x1)
