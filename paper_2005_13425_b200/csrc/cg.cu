@@ -328,8 +328,11 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         const Row<N> rw = make_row<N>(row, bf);
         const int64_t base = rw.e * NNN + rw.jk * N;
         double v[N], rv[N];
-        dssum_row<N>(w, rw, bx, DIST ? bot : nullptr, DIST ? top : nullptr, v);
+        // the r row first: its loads are independent of the ordered sum, so
+        // they share the first round trip with the w copies instead of
+        // following the sum's additions
         load_row_rw<N>(r + base, rv);
+        dssum_row<N>(w, rw, bx, DIST ? bot : nullptr, DIST ? top : nullptr, v);
 #pragma unroll
         for (int i = 0; i < N; ++i) {
             rv[i] = add_rn(rv[i], mul_rn(nalpha, mul_rn(v[i], row_mask<N>(rw, i))));
