@@ -26,6 +26,8 @@ for n in (3, 4, 6, 7, 8, 10, 11, 12, 14, 16):
     topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b, device=dev)
     f = sb.make_rhs(8, n, topo, sb.mix64(1, 8), device=dev)
     sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(4, 0.0))
+    if n in (7, 10):  # graph-replayed iterations with programmatic launches
+        sb.cg_solve(f, sb.GlobalOperator(geom, b, topo), topo, sb.CgConfig(25, 0.0))
     sb.cg_solve(f, lambda x: sb.apply_global(x, geom, b, topo), topo, sb.CgConfig(3, 0.0))
     sb.weighted_dot(f, f, topo)
 # large-n tilings with the wave-ahead u prefetch need more elements than one
