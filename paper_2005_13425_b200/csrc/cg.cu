@@ -287,7 +287,7 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
                   sem_cg_state* st, double* history, ReduceScratch* rs,
                   const double* __restrict__ bot, const double* __restrict__ top,
                   bool deferred = false, const double* __restrict__ gathered = nullptr,
-                  int nranks = 0)
+                  int nranks = 0, int reverse = 0)
 {
     constexpr int NN = N * N, NNN = N * N * N;
     SEM_TRACE_ENTRY(st);
@@ -322,8 +322,14 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     }
     const double nalpha = -alpha;
     double acc = 0.0;
-    for (int64_t row = (int64_t)blockIdx.x * RT + threadIdx.x; row < E * NN;
-         row += (int64_t)gridDim.x * RT) {
+    // reverse: walk the rows from the last element down, so the first rows
+    // updated are those of the elements the Ax launch processed LAST (their
+    // w and r still in L2) and the last rows written are the first elements
+    // the next Ax launch reads (r still in L2)
+    const int64_t nrows = E * NN;
+    for (int64_t q = (int64_t)blockIdx.x * RT + threadIdx.x; q < nrows;
+         q += (int64_t)gridDim.x * RT) {
+        const int64_t row = reverse ? nrows - 1 - q : q;
         const Box& bx = bf.b;
         const Row<N> rw = make_row<N>(row, bf);
         const int64_t base = rw.e * NNN + rw.jk * N;
@@ -612,6 +618,18 @@ cg_settle_kernel(const double* __restrict__ partials, int count, sem_cg_state* s
     else fin_phase(st, PH, tot, history);
 }
 
+// update row order (SEM_CG_UPD_REV: 1 (default) = last element first, 0 =
+// first element first).  The Ax launch walks the elements forward, so the
+// reversed update starts on the elements whose w and r are still in L2 and
+// finishes on the ones the next Ax reads first (tools/cg_ab.py with idle
+// gaps, profiles/r02_cg_graph_pdl.txt: E = 4096 94.3-96.1 -> 93.4-93.8 us,
+// E = 32768 unchanged)
+static int upd_rev()
+{
+    static const int k = getenv("SEM_CG_UPD_REV") ? atoi(getenv("SEM_CG_UPD_REV")) : 1;
+    return k;
+}
+
 // <p, A p> settle: 1 (default) a one-block settle launch after the Ax
 // launch, 0 folded into every update CTA (SEM_CG_SETTLE)
 static int settle_launch()
@@ -724,11 +742,13 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
             if (int rc = chk(rt256 ? launch_k(cg_update2_kernel<N, false, 256>, dim3(ug), dim3(256), 0, s,
                                               pdl, (const double*)w, r, E, make_box_flat(bx), st,
                                               history, rs, (const double*)nullptr,
-                                              (const double*)nullptr, true, (const double*)nullptr, 0)
+                                              (const double*)nullptr, true, (const double*)nullptr, 0,
+                                              upd_rev())
                                    : launch_k(cg_update2_kernel<N, false>, dim3(ug), dim3(kRowThreads), 0,
                                               s, pdl, (const double*)w, r, E, make_box_flat(bx), st,
                                               history, rs, (const double*)nullptr,
-                                              (const double*)nullptr, true, (const double*)nullptr, 0),
+                                              (const double*)nullptr, true, (const double*)nullptr, 0,
+                                              upd_rev()),
                              "cg update kernel"))
                 return rc;
             if (int rc = chk(launch_k(cg_settle_kernel<2>, dim3(1), dim3(kSettleThreads), 0, s, pdl,
@@ -741,11 +761,13 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
             if (int rc = chk(rt256 ? launch_k(cg_update2_kernel<N, false, 256>, dim3(upd_grid<N, 256>(E)),
                                               dim3(256), 0, s, pdl, (const double*)w, r, E,
                                               make_box_flat(bx), st, history, rs,
-                                              (const double*)nullptr, (const double*)nullptr, false, gath, ng)
+                                              (const double*)nullptr, (const double*)nullptr, false, gath, ng,
+                                              upd_rev())
                                    : launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
                                               dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E,
                                               make_box_flat(bx), st, history, rs,
-                                              (const double*)nullptr, (const double*)nullptr, false, gath, ng),
+                                              (const double*)nullptr, (const double*)nullptr, false, gath, ng,
+                                              upd_rev()),
                              "cg update kernel"))
                 return rc;
         }

@@ -59,6 +59,7 @@ MODES = {
     "updelem": {"SEM_CG_UPD_ELEM": "1"},
     "settle0": {"SEM_CG_SETTLE": "0"},
     "settle1": {"SEM_CG_SETTLE": "1"},
+    "updfwd": {"SEM_CG_UPD_REV": "0"},
 }
 
 
