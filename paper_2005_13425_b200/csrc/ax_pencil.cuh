@@ -254,6 +254,8 @@ struct CgpArgs {
     unsigned* grid_out;   // host side: the launch's grid size (may be null)
     int pdl;              // launched as a programmatic dependent (GMODE 4: the
                           // metric copy is issued before griddep_wait)
+    int reverse = 0;      // CGM == 2: CTA b processes element E-1-b (the
+                          // iteration walks the elements backward)
 };
 
 // Doubles of layer stacks per slot: U, A, B -- or U and A only when B
@@ -314,7 +316,8 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     const int jp_i = p % N, jp_k = p / N;          // j-pencil (i,k): p = k*N + i
 
     const int64_t nbatches = (num_elements + SLOTS - 1) / SLOTS;
-    int64_t batch = blockIdx.x;
+    int64_t batch = (CGM == 2 && !PERSIST && cgp.reverse) ? nbatches - 1 - (int64_t)blockIdx.x
+                                                           : (int64_t)blockIdx.x;
     // PERSIST: grid-stride over batches with the next batch's u prefetched;
     // otherwise one batch per CTA (D constants are not loop-invariant, so
     // the compiler keeps them in uniform registers only around their use).
@@ -531,8 +534,9 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             if (pf_elems > 0 && e + pf_elems < num_elements)
                 prefetch_l2_bulk(u, (e + pf_elems) * NNN * 8, (e + pf_elems + 1) * NNN * 8,
                                  num_elements * NNN * 8);
-        } else if (L2PF && pf_elems >= 0 && lane_ok && p == 0 && e + pf_elems < num_elements) {
-            const int64_t en = e + pf_elems;
+        } else if (L2PF && pf_elems >= 0 && lane_ok && p == 0 &&
+                   (CGM == 2 && cgp.reverse ? e - pf_elems >= 0 : e + pf_elems < num_elements)) {
+            const int64_t en = (CGM == 2 && cgp.reverse) ? e - pf_elems : e + pf_elems;
             prefetch_l2_bulk(u, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);
             if constexpr (CGM != 0) {
                 prefetch_l2_bulk(cgp.r, en * NNN * 8, (en + 1) * NNN * 8, num_elements * NNN * 8);

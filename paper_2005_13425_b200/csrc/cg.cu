@@ -618,6 +618,19 @@ cg_settle_kernel(const double* __restrict__ partials, int count, sem_cg_state* s
     else fin_phase(st, PH, tot, history);
 }
 
+// alternate the element walk direction every iteration (SEM_CG_ALT: 1
+// default): even iterations run the Ax launch forward and the update
+// backward, odd ones the Ax backward (it starts on the metric blocks and
+// vectors the previous Ax ended on, which the update's ~100 MB left partly
+// in L2) and the update forward.  tools/cg_ab.py, 8 idle-gapped solves per
+// setting on one box (profiles/r02_cg_graph_pdl.txt): E = 4096 median
+// 96.9 -> 94.2 us; E = 32768 unchanged.
+static int cg_alt()
+{
+    static const int k = getenv("SEM_CG_ALT") ? atoi(getenv("SEM_CG_ALT")) : 1;
+    return k;
+}
+
 // update row order (SEM_CG_UPD_REV: 1 (default) = last element first, 0 =
 // first element first).  The Ax launch walks the elements forward, so the
 // reversed update starts on the elements whose w and r are still in L2 and
@@ -726,7 +739,13 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
     auto chk = [](cudaError_t e, const char* what) { return e == cudaSuccess ? 0 : fail_cuda(e, what); };
     for (int it = 0; it < iters; ++it) {
         if (cudaError_t e = mark(3 * it)) return fail_cuda(e, "sem_cg_run: event");
-        if (int rc = ax_cg_dispatch(g, dx, w, E, N, a, 2, s)) return rc;
+        // SEM_CG_ALT: odd iterations walk the elements backward (the Ax
+        // launch starts on the metric the previous Ax left in L2) and their
+        // update forward
+        CgpArgs ai = a;
+        ai.reverse = (cg_alt() && (it & 1)) ? 1 : 0;
+        const int urev = cg_alt() ? ((it & 1) ? 0 : 1) : upd_rev();
+        if (int rc = ax_cg_dispatch(g, dx, w, E, N, ai, 2, s)) return rc;
         const bool fold = defer_ax && !defer && !settle_launch() && !upd_elem();
         if (defer_ax && !fold) {
             if (int rc = chk(launch_k(cg_settle_kernel<kPhasePap>, dim3(1), dim3(kSettleThreads), 0, s,
@@ -743,12 +762,12 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
                                               pdl, (const double*)w, r, E, make_box_flat(bx), st,
                                               history, rs, (const double*)nullptr,
                                               (const double*)nullptr, true, (const double*)nullptr, 0,
-                                              upd_rev())
+                                              urev)
                                    : launch_k(cg_update2_kernel<N, false>, dim3(ug), dim3(kRowThreads), 0,
                                               s, pdl, (const double*)w, r, E, make_box_flat(bx), st,
                                               history, rs, (const double*)nullptr,
                                               (const double*)nullptr, true, (const double*)nullptr, 0,
-                                              upd_rev()),
+                                              urev),
                              "cg update kernel"))
                 return rc;
             if (int rc = chk(launch_k(cg_settle_kernel<2>, dim3(1), dim3(kSettleThreads), 0, s, pdl,
@@ -762,12 +781,12 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
                                               dim3(256), 0, s, pdl, (const double*)w, r, E,
                                               make_box_flat(bx), st, history, rs,
                                               (const double*)nullptr, (const double*)nullptr, false, gath, ng,
-                                              upd_rev())
+                                              urev)
                                    : launch_k(cg_update2_kernel<N, false>, dim3(upd_grid<N>(E)),
                                               dim3(kRowThreads), 0, s, pdl, (const double*)w, r, E,
                                               make_box_flat(bx), st, history, rs,
                                               (const double*)nullptr, (const double*)nullptr, false, gath, ng,
-                                              upd_rev()),
+                                              urev),
                              "cg update kernel"))
                 return rc;
         }

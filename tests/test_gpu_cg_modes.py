@@ -60,6 +60,7 @@ MODES = {
     "settle0": {"SEM_CG_SETTLE": "0"},
     "settle1": {"SEM_CG_SETTLE": "1"},
     "updfwd": {"SEM_CG_UPD_REV": "0"},
+    "noalt": {"SEM_CG_ALT": "0"},
 }
 
 
