@@ -185,6 +185,16 @@ int sem_cg_run(const double *g, const double *dx, const double *dxt, double *x,
                double *r, double *p, double *w, sem_cg_state *state, double *history,
                int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,
                void *scratch, sem_stream_t stream);
+/* sem_cg_run for iterations first_iteration .. first_iteration+iterations-1
+ * of a solve (1-based): the fused iteration alternates its element walk
+ * direction by the parity of the global iteration number (L2 reuse between
+ * consecutive Ax launches), so a solve split into several calls -- one per
+ * callback, graph replays of a fixed chunk -- rounds exactly like one call.
+ * sem_cg_run(...) == sem_cg_run_at(..., first_iteration = 1, ...). */
+int sem_cg_run_at(const double *g, const double *dx, const double *dxt, double *x,
+                  double *r, double *p, double *w, sem_cg_state *state, double *history,
+                  int32_t iterations, int32_t first_iteration, int32_t ex, int32_t ey,
+                  int32_t ez, int32_t n, void *scratch, sem_stream_t stream);
 /* Apply the pending x += alpha p (if any; not after a breakdown) and clear it.
  * num_points = E*n^3. */
 int sem_cg_finalize(double *x, const double *p, sem_cg_state *state, int64_t num_points,

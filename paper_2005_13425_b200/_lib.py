@@ -74,6 +74,8 @@ SIGNATURES = {
                                    _i32, _vp, _vp]),
     "sem_cg_run": (ctypes.c_int, [_vp, _dp, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,
                                   _i32, _i32, _vp, _vp]),
+    "sem_cg_run_at": (ctypes.c_int, [_vp, _dp, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
+                                     _i32, _i32, _i32, _i32, _vp, _vp]),
     "sem_cg_finalize": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "sem_cg_run_phases": (ctypes.c_int, [_vp, _dp, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
                                          _i32, _i32, _i32, _vp, _dp, _vp]),

@@ -201,12 +201,14 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
 
     win = _l2_window(ws, s)
 
-    def run(k: int):
-        # stream looked up at call time: inside graph capture it is the capture stream
-        check(lib.sem_cg_run(dv.ptr(g), dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt), dv.ptr(ws.x),
-                             dv.ptr(ws.r), dv.ptr(ws.p), dv.ptr(ws.w), dv.ptr(ws.state),
-                             dv.ptr(ws.history), k, *box, dv.ptr(ws.scratch),
-                             dv.stream_handle(dev)), "cg_solve run")
+    def run(k: int, first: int):
+        # iterations first .. first+k-1 (1-based, global: the kernels alternate
+        # their element walk by its parity).  The stream is looked up at call
+        # time: inside graph capture it is the capture stream.
+        check(lib.sem_cg_run_at(dv.ptr(g), dv.host_f64_ptr(dx), dv.host_f64_ptr(dxt),
+                                dv.ptr(ws.x), dv.ptr(ws.r), dv.ptr(ws.p), dv.ptr(ws.w),
+                                dv.ptr(ws.state), dv.ptr(ws.history), k, first, *box,
+                                dv.ptr(ws.scratch), dv.stream_handle(dev)), "cg_solve run")
 
     m = ws.x.numel()
 
@@ -231,7 +233,7 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
         finalize()
         st = ws.read_state()
     elif callback is None:
-        if cfg.max_iterations > max(2, GRAPH_ITERATIONS) and USE_GRAPHS:
+        if cfg.max_iterations > max(2, GRAPH_ITERATIONS + 1) and USE_GRAPHS:
             # iteration 1 launched directly (configures the kernels), then
             # GRAPH_ITERATIONS iterations are captured into one CUDA graph and
             # replayed: the launches are parameter-stable (scalars live in the
@@ -240,13 +242,15 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
             # host also polls the stop flag without blocking (an async copy
             # into pinned memory every POLL_EVERY replays, read once its event
             # has completed) and stops replaying once the solve has ended.
-            run(1)
+            run(1, 1)
             rest = cfg.max_iterations - 1
             # always the same graph size (a short solve runs its iterations
-            # directly instead of capturing -- and evicting -- another graph)
-            k = max(1, GRAPH_ITERATIONS)
+            # directly instead of capturing -- and evicting -- another graph);
+            # even, so every replay starts on an even global iteration, the
+            # parity the graph was captured with
+            k = max(2, GRAPH_ITERATIONS + (GRAPH_ITERATIONS & 1))
             key = (g.data_ptr(), box, dx.tobytes(), k)
-            graph = ws.iteration_graph(lambda: run(k), key)
+            graph = ws.iteration_graph(lambda: run(k, 2), key)
             stream = torch.cuda.current_stream(dev)
             ws._stop_host.zero_()
             ws._stop_event = None
@@ -262,15 +266,15 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
                     ws._stop_event.record(stream)
             else:
                 if rest % k:
-                    run(rest % k)
+                    run(rest % k, 2 + (rest // k) * k)
         else:
-            run(cfg.max_iterations)
+            run(cfg.max_iterations, 1)
         finalize()
         st = ws.read_state()
     else:
         st = None
         for it in range(1, cfg.max_iterations + 1):
-            run(1)
+            run(1, it)
             finalize()
             st = ws.read_state()
             if st.iterations_run >= it and st.stop != 2:

@@ -720,7 +720,7 @@ template <int N>
 static int cg_run_n(const double* g, const double* dx, double* x, double* r, double* p,
                     double* w, double* w2, sem_cg_state* st, double* history, int iters,
                     int64_t E, Box bx, ReduceScratch* rs, cudaStream_t s,
-                    cudaEvent_t* marks = nullptr)
+                    cudaEvent_t* marks = nullptr, int first_it = 1)
 {
     // marks (optional, 3*iters+1 events): recorded before each iteration's
     // Ax, assemble and update launches and after the last one
@@ -742,9 +742,13 @@ static int cg_run_n(const double* g, const double* dx, double* x, double* r, dou
         // SEM_CG_ALT: odd iterations walk the elements backward (the Ax
         // launch starts on the metric the previous Ax left in L2) and their
         // update forward
+        // (parity of the GLOBAL 1-based iteration number, so any split of a
+        // solve into sem_cg_run_at calls -- eager, graph-replayed, one per
+        // callback -- walks the same way and rounds identically)
+        const bool back = ((first_it + it) % 2) == 0;
         CgpArgs ai = a;
-        ai.reverse = (cg_alt() && (it & 1)) ? 1 : 0;
-        const int urev = cg_alt() ? ((it & 1) ? 0 : 1) : upd_rev();
+        ai.reverse = (cg_alt() && back) ? 1 : 0;
+        const int urev = cg_alt() ? (back ? 0 : 1) : upd_rev();
         if (int rc = ax_cg_dispatch(g, dx, w, E, N, ai, 2, s)) return rc;
         const bool fold = defer_ax && !defer && !settle_launch() && !upd_elem();
         if (defer_ax && !fold) {
@@ -881,13 +885,18 @@ extern "C" int sem_cg_init(const double* f, double* x, double* r, double* p, sem
                                          tolerance, s));
 }
 
-extern "C" int sem_cg_run(const double* g, const double* dx, const double* dxt, double* x,
-                          double* r, double* p, double* w, sem_cg_state* state, double* history,
-                          int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,
-                          void* scratch, sem_stream_t stream)
+extern "C" int sem_cg_run_at(const double* g, const double* dx, const double* dxt, double* x,
+                             double* r, double* p, double* w, sem_cg_state* state,
+                             double* history, int32_t iterations, int32_t first_iteration,
+                             int32_t ex, int32_t ey, int32_t ez, int32_t n, void* scratch,
+                             sem_stream_t stream)
 {
     (void)dxt;
     if (int rc = check_box(ex, ey, ez, n, "sem_cg_run")) return rc;
+    if (first_iteration < 1) {
+        set_error("sem_cg_run_at: first_iteration is 1-based");
+        return SEM_E_INVALID;
+    }
     if (!g || !dx || !x || !r || !p || !w || !state || !history || !scratch || iterations < 0) {
         set_error("sem_cg_run: bad arguments");
         return SEM_E_INVALID;
@@ -906,7 +915,16 @@ extern "C" int sem_cg_run(const double* g, const double* dx, const double* dxt, 
     double* w_local = w;
     double* w_asm = w + m + (m & 1);
     SEM_SWITCH_N(n, return cg_run_n<NV>(g, dx, x, r, p, w_local, w_asm, state, history,
-                                        iterations, E, bx, rs, s));
+                                        iterations, E, bx, rs, s, nullptr, first_iteration));
+}
+
+extern "C" int sem_cg_run(const double* g, const double* dx, const double* dxt, double* x,
+                          double* r, double* p, double* w, sem_cg_state* state, double* history,
+                          int32_t iterations, int32_t ex, int32_t ey, int32_t ez, int32_t n,
+                          void* scratch, sem_stream_t stream)
+{
+    return sem_cg_run_at(g, dx, dxt, x, r, p, w, state, history, iterations, 1, ex, ey, ez, n,
+                         scratch, stream);
 }
 
 extern "C" int sem_cg_finalize(double* x, const double* p, sem_cg_state* state,
