@@ -30,9 +30,11 @@ for rep in range(int(os.environ.get("CG_REPS", "3"))):
         ws = sb.CgWorkspace(topo, iters, dev)
         sb.cg_solve(f, op, topo, sb.CgConfig(iters, 0.0), workspace=ws)  # capture + warm
         torch.cuda.synchronize()
-        time.sleep(1.0)
+        time.sleep(float(os.environ.get("CG_IDLE", "1.0")))
         best = None
         for _ in range(3):
+            if os.environ.get("CG_WARM"):  # a short burst of iterations first
+                sb.cg_solve(f, op, topo, sb.CgConfig(int(os.environ["CG_WARM"]), 0.0), workspace=ws)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             sb.cg_solve(f, op, topo, sb.CgConfig(iters, 0.0), workspace=ws)
