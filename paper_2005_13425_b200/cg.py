@@ -130,12 +130,19 @@ class CgWorkspace:
         # pinned mirror of state.stop for the replay loop's non-blocking poll
         self._stop_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self._stop_event = None
+        self._poll_stream = None
 
     def fits(self, topo: Topology, max_iterations: int, device: torch.device) -> bool:
         """Usable for a solve on `topo` (same box and n: the launches index the
         vectors by the box) with this iteration budget on this device."""
         return (self.box == (topo.ex, topo.ey, topo.ez, topo.n)
                 and self.max_iterations >= max_iterations and self.device == device)
+
+    def poll_stream(self) -> torch.cuda.Stream:
+        """Side stream for the non-blocking stop-flag copies."""
+        if self._poll_stream is None:
+            self._poll_stream = torch.cuda.Stream(self.device)
+        return self._poll_stream
 
     def iteration_graph(self, launch_one, key):
         """CUDA graph of one fused iteration (captured once per workspace and
@@ -260,10 +267,18 @@ def _fused_solve(f_dev: torch.Tensor, op: GlobalOperator, topo: Topology, cfg: C
                     if ws._stop_event is not None and ws._stop_event.query() \
                             and int(ws._stop_host[0]) != 0:
                         break
-                    ws._stop_host.copy_(ws.state[_STOP_OFFSET:_STOP_OFFSET + 4]
-                                        .view(torch.int32), non_blocking=True)
+                    # the flag is copied on a side stream that waits for this
+                    # replay: a copy on the solve's own stream would sit
+                    # between two replays (~1% of an E = 4096 iteration)
+                    done = torch.cuda.Event()
+                    done.record(stream)
+                    ps = ws.poll_stream()
+                    ps.wait_event(done)
+                    with torch.cuda.stream(ps):
+                        ws._stop_host.copy_(ws.state[_STOP_OFFSET:_STOP_OFFSET + 4]
+                                            .view(torch.int32), non_blocking=True)
                     ws._stop_event = torch.cuda.Event()
-                    ws._stop_event.record(stream)
+                    ws._stop_event.record(ps)
             else:
                 if rest % k:
                     run(rest % k, 2 + (rest // k) * k)
