@@ -90,13 +90,19 @@ def weighted_dot(u, v, topo) -> float:
         return float(out.item())
 
 
-def _consistent(f_dev: torch.Tensor, topo: Topology) -> bool:
-    """Is mask(f) interface-consistent (equal copies of every shared node)?"""
+def _consistency_flag(f_dev: torch.Tensor, topo: Topology) -> torch.Tensor:
+    """Device int32: 0 iff mask(f) is interface-consistent (equal copies of
+    every shared node).  Enqueued only -- nothing waits on it here."""
     flag = torch.empty(1, dtype=torch.int32, device=f_dev.device)
     check(load().sem_consistent_box(dv.ptr(f_dev), topo.ex, topo.ey, topo.ez, topo.n,
                                     dv.ptr(flag), dv.stream_handle(f_dev.device)),
           "cg_solve consistency check")
-    return int(flag.item()) == 0
+    return flag
+
+
+def _consistent(f_dev: torch.Tensor, topo: Topology) -> bool:
+    """Is mask(f) interface-consistent (equal copies of every shared node)?"""
+    return int(_consistency_flag(f_dev, topo).item()) == 0
 
 
 class CgWorkspace:
@@ -418,10 +424,27 @@ def cg_solve(f, operator, topo, cfg: CgConfig,
     counters.add(reads=2 * dofs, writes=dofs)
     with torch.cuda.device(fd.device):
         fused = (isinstance(operator, GlobalOperator) and isinstance(topo, Topology)
-                 and operator.topo == topo and _consistent(fd, topo))
-        if fused:
-            x, history, iters, zero_exit = _fused_solve(fd, operator, topo, cfg, callback, host,
-                                                        workspace)
+                 and operator.topo == topo)
+        out = None
+        if fused and callback is None:
+            # optimistic: the consistency check is enqueued ahead of the fused
+            # solve and read once the solve's own final synchronisation has
+            # happened (no host round trip before the first launch); an
+            # inconsistent rhs -- rare, the fused <p, A p> assumes a
+            # continuous p -- discards the result and takes the generic path
+            flag = _consistency_flag(fd, topo)
+            try:
+                out = _fused_solve(fd, operator, topo, cfg, callback, host, workspace)
+            except CgBreakdownError:
+                if int(flag.item()) == 0:
+                    raise
+                out = None
+            if out is not None and int(flag.item()) != 0:
+                out = None
+        elif fused and _consistent(fd, topo):  # callbacks see every iterate: check first
+            out = _fused_solve(fd, operator, topo, cfg, callback, host, workspace)
+        if out is not None:
+            x, history, iters, zero_exit = out
             full = iters - (1 if zero_exit else 0)
             counters.add(reads=15 * dofs * full, writes=3 * dofs * full,
                          flops=CG_VECTOR_FLOPS_PER_POINT * dofs * full)

@@ -44,3 +44,23 @@ gc.enable()
 C.POLL_EVERY = 10 ** 9
 run("no_poll")
 C.POLL_EVERY = 8
+
+# fixed per-solve cost: solves of 12 and 112 iterations (both graph-replayed)
+def solve_ms(it):
+    best = None
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sb.cg_solve(f, op, topo, sb.CgConfig(it, 0.0), workspace=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    return best
+
+
+ws = sb.CgWorkspace(topo, 112, dev)
+sb.cg_solve(f, op, topo, sb.CgConfig(112, 0.0), workspace=ws)
+a, b2 = solve_ms(12), solve_ms(112)
+per_it = (b2 - a) / 100
+print(json.dumps({"per_iteration_us": round(per_it * 1e3, 2), "fixed_per_solve_us": round((a - 12 * per_it) * 1e3, 1)}))
