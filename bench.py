@@ -805,6 +805,26 @@ def bench_cg(sb, dev, iters):
         torch.cuda.synchronize(dev)
         solves.append(e0.elapsed_time(e1))
     ms = statistics.median(solves)
+    # steady-state cost of one iteration: the difference between solves of
+    # iters + GRAPH_ITERATIONS and GRAPH_ITERATIONS + 2 iterations (the
+    # fixed per-solve host / launch / synchronisation cost cancels)
+    from paper_2005_13425_b200 import cg as C
+    lengths = (C.GRAPH_ITERATIONS + 2, iters + C.GRAPH_ITERATIONS + 2)
+    ws_long = sb.CgWorkspace(topo, lengths[1], dev)
+    sb.cg_solve(f, op, topo, sb.CgConfig(lengths[1], 0.0), workspace=ws_long)
+    t_len = []
+    for L in lengths:
+        best = None
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            sb.cg_solve(f, op, topo, sb.CgConfig(L, 0.0), workspace=ws_long)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            t = e0.elapsed_time(e1)
+            best = t if best is None else min(best, t)
+        t_len.append(best)
+    steady_ms = (t_len[1] - t_len[0]) / (lengths[1] - lengths[0])
     dofs = topo.dofs
     per_it = ms / iters
     model_flops = perf.model_flops_per_iteration(dofs, n)
@@ -817,6 +837,9 @@ def bench_cg(sb, dev, iters):
             "paper_roofline_frac": gf / perf.roofline_peak(hbm, n),
             "design_bytes_per_iteration": design_bytes,
             "design_roofline_frac": design_bytes / (per_it * 1e-3) / hbm,
+            "steady_ms_per_iteration": steady_ms,
+            "steady_design_roofline_frac": design_bytes / (steady_ms * 1e-3) / hbm,
+            "fixed_ms_per_solve": ms - steady_ms * iters,
             "final_residual": float(res.residual_history[-1]),
             "note": "paper Eq.(1)/(2) model: D(12n+34) flop, 240 D bytes per iteration; "
                     "timed with CUDA events incl. one host sync at the end, median of 5 "
