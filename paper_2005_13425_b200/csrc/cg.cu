@@ -293,7 +293,10 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     SEM_TRACE_ENTRY(st);
     griddep_wait();
     SEM_TRACE_WAITED(st);
-    if (st->stop) return;
+    // both state fields in one round trip (loaded before the stop branch)
+    const int st_stop = st->stop;
+    const double st_alpha = st->alpha;
+    if (st_stop) return;
     double alpha;
     if (DIST && gathered != nullptr) {
         // multi-GPU phase-1 finish folded in: every CTA combines the ranks'
@@ -318,7 +321,7 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         if (pap_s <= 0.0) return;  // breakdown (block 0 set stop = 2)
         alpha = ldexp(st->rtz, 2 * pap_scale_exp(st->rtz)) / pap_s;
     } else {
-        alpha = st->alpha;
+        alpha = st_alpha;
     }
     const double nalpha = -alpha;
     double acc = 0.0;

@@ -30,7 +30,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 SCRIPT = r"""
-import json, sys
+import json, os, sys
 sys.path.insert(0, {root!r})
 import paper_2005_13425_b200 as sb
 n, (ex, ey, ez) = 10, (6, 5, 4)
@@ -40,12 +40,13 @@ topo, geom = sb.build_topology(mesh), sb.build_geom(mesh, b)
 E = mesh.num_elements
 f = sb.make_rhs(E, n, topo, sb.mix64(1, E))
 op = sb.GlobalOperator(geom, b, topo)
+tol = float(os.environ.get("CG_TEST_TOL", "0"))
 out = []
 for _ in range(2):
-    res = sb.cg_solve(f, op, topo, sb.CgConfig(40, 0.0))
+    res = sb.cg_solve(f, op, topo, sb.CgConfig(40, tol))
     out.append([float(v) for v in res.residual_history])
 x = res.solution
-print(json.dumps({{"hist": out, "xsum": float(abs(x).sum())}}))
+print(json.dumps({{"hist": out, "xsum": float(abs(x).sum()), "iters": int(res.iterations_run)}}))
 """
 
 MODES = {
@@ -108,3 +109,25 @@ def test_cg_modes_same_trees_bitexact(runs):
     base = runs["default"]["hist"][0]
     for mode in ("pdl0", "pdl1", "axcfg4"):
         assert runs[mode]["hist"][0] == base, mode
+
+
+def test_cg_tolerance_exit_mid_graph(cuda, oracle_hist):
+    # a tolerance first met at iteration 23 (inside the third 10-iteration
+    # graph): the stop flag turns the rest of the graph into no-ops -- same
+    # iteration count and history as the oracle's early exit
+    import oracle as O
+    import paper_2005_13425_b200 as sb
+    tol = float(oracle_hist[22]) * (1.0 + 1e-6)
+    assert tol < float(np.min(oracle_hist[:22]))
+    r = _run({"CG_TEST_TOL": repr(tol)})
+    n, (ex, ey, ez) = 10, (6, 5, 4)
+    b = sb.build_basis(n)
+    T = O.BoxTopology(ex, ey, ez, n)
+    g = O.box_geom(ex, ey, ez, b.weights, 1.0)
+    E = ex * ey * ez
+    f0 = O.random_field(E, n, O.mix64(1, E))
+    f = O.mask(O.dssum(f0, T), T)
+    _, hist, _ = O.cg(f, lambda p: O.apply_global(p, g, b.diff, b.diff_t, T), T, 40, tol)
+    h = np.asarray(r["hist"][0])
+    assert r["iters"] == len(hist) == 23
+    assert float(np.max(np.abs(h - hist) / np.abs(hist))) <= 1e-10
