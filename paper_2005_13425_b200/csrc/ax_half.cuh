@@ -80,8 +80,9 @@ template <int N, int MINB, int PD, bool FOLD>
 __global__ void __launch_bounds__(HalfCfg<N>::THREADS, MINB)
 ax_half_kernel(const double* __restrict__ u, const double* __restrict__ g,
                double* __restrict__ w, int64_t num_elements, const DParamP<N> D,
-               int64_t uahead = 0)
+               int64_t uahead = 0, int stagger_ns = 0, int stagger_lo = 0, int stagger_hi = 0)
 {
+    stagger_wait(stagger_ns, stagger_lo, stagger_hi);
     using C = HalfCfg<N>;
     constexpr int NN = C::NN, NNN = C::NNN, KH = C::KH, LSU = C::LSU, LSA = C::LSA,
                   LSB = C::LSB, NP = C::NP, RS = C::RS;

@@ -26,6 +26,7 @@
 // Arithmetic differs from the reference only by FMA contraction and
 // association (tolerance 1e-12 max-norm relative, sembench/verify.py:37-42).
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <atomic>
@@ -338,6 +339,24 @@ static bool fill_dparam_compute(DParamP<N>& P, const double* dx)
     return dev <= 1e-13 * scale;
 }
 
+// Phase stagger of the large-n kernels (stagger_wait): the second CTA of
+// every SM waits kStaggerNs[N] at entry when the launch has several waves
+// (nbatches >= 4 x resident).  SEM_AX_STAGGER=ns[,lo,hi] overrides (tuning).
+constexpr int kStaggerNs[17] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+template <int N>
+static void stagger_cfg(int minb, int64_t nbatches, int& ns, int& lo, int& hi)
+{
+    static const char* env = getenv("SEM_AX_STAGGER");
+    ns = 0;
+    lo = sm_count();
+    hi = 2 * sm_count();
+    if (env) {
+        sscanf(env, "%d,%d,%d", &ns, &lo, &hi);
+        return;
+    }
+    if (minb == 2 && nbatches >= 4 * (int64_t)minb * sm_count()) ns = kStaggerNs[N];
+}
+
 template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0, int GMODE = 0,
           bool FOLD = false, int CGM = 0, bool ALIAS = false, bool WBULK = false>
 static int launch_pencil(const double* u, const double* g, const double* dx, double* w,
@@ -389,6 +408,9 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     static const char* pf_env = getenv("SEM_AX_PFDIST");  // tuning probe
     if (pf_env) pf = atoll(pf_env);
     if (cgp.grid_out) *cgp.grid_out = (unsigned)grid;
+    if constexpr (CGM == 0) {
+        if (!PERSIST) stagger_cfg<N>(MINB, nbatches, cgp.stagger_ns, cgp.stagger_lo, cgp.stagger_hi);
+    }
     // plain Ax as a programmatic dependent (CGM == 0): the pre-wait L2
     // prefetch of the CTA's own blocks (pdl == 2) pays for short launches and
     // cost ~0.6% on long ones (E = 1024: 13.2 -> 12.9 us; E = 4096: 41.7 ->
@@ -458,8 +480,11 @@ static int launch_half(const double* u, const double* g, const double* dx, doubl
             configured.fetch_or(bit, std::memory_order_release);
         }
         const int64_t resident = (int64_t)sm_count() * MINB;
+        int sns = 0, slo = 0, shi = 0;
+        stagger_cfg<N>(MINB, E, sns, slo, shi);
         kern<<<(unsigned)E, C::THREADS, C::SMEM, stream>>>(u, g, w, E, D,
-                                                           uahead && E > resident ? resident : 0);
+                                                           uahead && E > resident ? resident : 0, sns,
+                                                           slo, shi);
         SEM_CHECK_LAUNCH("sem_ax (half-pencil) launch");
         return 0;
     }

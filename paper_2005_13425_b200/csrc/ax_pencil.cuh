@@ -256,6 +256,9 @@ struct CgpArgs {
                           // metric copy is issued before griddep_wait)
     int reverse = 0;      // CGM == 2: CTA b processes element E-1-b (the
                           // iteration walks the elements backward)
+    // CGM == 0: CTAs stagger_lo..stagger_hi-1 wait stagger_ns at entry
+    // (stagger_wait, large n)
+    int stagger_ns = 0, stagger_lo = 0, stagger_hi = 0;
 };
 
 // Doubles of layer stacks per slot: U, A, B -- or U and A only when B
@@ -322,6 +325,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     // otherwise one batch per CTA (D constants are not loop-invariant, so
     // the compiler keeps them in uniform registers only around their use).
 
+    if constexpr (CGM == 0) stagger_wait(cgp.stagger_ns, cgp.stagger_lo, cgp.stagger_hi);
     double beta = 0.0, alpha_prev = 0.0, pap_s = 1.0;
     bool xpend = false;
 #ifdef SEM_TRACE
@@ -387,12 +391,16 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     if constexpr (CGM != 0) {
         static_assert(!PERSIST && GMODE != 2, "CG fusion: one batch per CTA, p via registers or GMODE 4");
         sem_cg_state* st = cgp.st;
-        if (st->stop) {                             // uniform over the grid
+        // every state field this prologue uses is loaded up front, before
+        // the first branch: one round trip instead of the stop flag's and
+        // then the scalars'
+        const int st_stop = st->stop, st_it = st->it, st_xp = st->x_pending;
+        const double rtz = st->rtz, st_rtz_old = st->rtz_old, st_alpha = st->alpha;
+        if (st_stop) {                              // uniform over the grid
             drain();
             return;
         }
-        const int it = st->it + 1;
-        const double rtz = st->rtz;
+        const int it = st_it + 1;
         if (rtz == 0.0) {                            // cg.py:151-158
             if (blockIdx.x == 0 && tid == 0) {
                 cgp.history[it - 1] = 0.0;
@@ -402,10 +410,10 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
             drain();
             return;
         }
-        beta = (it == 1) ? 0.0 : rtz / st->rtz_old;
+        beta = (it == 1) ? 0.0 : rtz / st_rtz_old;
         pap_s = ldexp(1.0, pap_scale_exp(rtz));  // exact power of two (fin_pap)
-        xpend = st->x_pending != 0;
-        alpha_prev = st->alpha;
+        xpend = st_xp != 0;
+        alpha_prev = st_alpha;
         if (blockIdx.x == 0 && tid == 0) st->beta = beta;
     }
     double pap_acc = 0.0;
