@@ -416,6 +416,13 @@ static int launch_pencil(const double* u, const double* g, const double* dx, dou
     if (cgp.grid_out) *cgp.grid_out = (unsigned)grid;
     if constexpr (CGM == 0) {
         if (!PERSIST) stagger_cfg<N>(MINB, nbatches, cgp.stagger_ns, cgp.stagger_lo, cgp.stagger_hi);
+    } else if constexpr (CGM == 2) {  // tuning probe: SEM_CG_STAGGER=ns[,lo,hi]
+        static const char* cg_env = getenv("SEM_CG_STAGGER");
+        if (cg_env) {
+            cgp.stagger_lo = sm_count();
+            cgp.stagger_hi = 2 * sm_count();
+            sscanf(cg_env, "%d,%d,%d", &cgp.stagger_ns, &cgp.stagger_lo, &cgp.stagger_hi);
+        }
     }
     // plain Ax as a programmatic dependent (CGM == 0): the pre-wait L2
     // prefetch of the CTA's own blocks (pdl == 2) pays for short launches and

@@ -256,8 +256,8 @@ struct CgpArgs {
                           // metric copy is issued before griddep_wait)
     int reverse = 0;      // CGM == 2: CTA b processes element E-1-b (the
                           // iteration walks the elements backward)
-    // CGM == 0: CTAs stagger_lo..stagger_hi-1 wait stagger_ns at entry
-    // (stagger_wait, large n)
+    // CTAs stagger_lo..stagger_hi-1 wait stagger_ns at entry (stagger_wait:
+    // large-n plain Ax; CGM == 2 only under the SEM_CG_STAGGER probe)
     int stagger_ns = 0, stagger_lo = 0, stagger_hi = 0;
 };
 
@@ -325,7 +325,7 @@ ax_pencil_kernel(const double* __restrict__ u, const double* __restrict__ g,
     // otherwise one batch per CTA (D constants are not loop-invariant, so
     // the compiler keeps them in uniform registers only around their use).
 
-    if constexpr (CGM == 0) stagger_wait(cgp.stagger_ns, cgp.stagger_lo, cgp.stagger_hi);
+    if constexpr (CGM != 3) stagger_wait(cgp.stagger_ns, cgp.stagger_lo, cgp.stagger_hi);
     double beta = 0.0, alpha_prev = 0.0, pap_s = 1.0;
     bool xpend = false;
 #ifdef SEM_TRACE

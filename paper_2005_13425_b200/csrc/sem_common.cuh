@@ -53,20 +53,21 @@ __device__ __forceinline__ void griddep_launch()
 }
 
 // Phase stagger of co-resident CTAs (large-n Ax): CTAs lo..hi-1 -- the
-// second CTA of every SM in the first wave -- idle ns nanoseconds at entry.
-// The CTAs sharing an SM then run out of step: one streams its metric (S4)
-// while the other is in its shared-memory contractions, and every later CTA
-// inherits its slot's offset, so HBM demand is spread over the element
-// instead of arriving in per-wave bursts.
+// second CTA of every SM in the first wave -- idle at entry for ns
+// nanoseconds at the 1965 MHz boost clock, counted in SM cycles (clock64) so
+// the offset stays the same fraction of an element's time when the power cap
+// lowers the clock.  The CTAs sharing an SM then run out of step: one
+// streams its metric (S4) while the other is in its shared-memory
+// contractions, and every later CTA inherits its slot's offset, so HBM
+// demand is spread over the element instead of arriving in per-wave bursts.
 __device__ __forceinline__ void stagger_wait(int ns, int lo, int hi)
 {
     if (ns <= 0 || (int)blockIdx.x < lo || (int)blockIdx.x >= hi) return;
-    unsigned long long t0, t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const long long cycles = (long long)ns * 1965 / 1000;
+    const long long t0 = clock64();
     do {
         __nanosleep(256);
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    } while (t - t0 < (unsigned long long)ns);
+    } while (clock64() - t0 < cycles);
 }
 
 // Timeline tracing of the fused CG chain (diagnostic builds only,
