@@ -339,28 +339,29 @@ static bool fill_dparam_compute(DParamP<N>& P, const double* dx)
     return dev <= 1e-13 * scale;
 }
 
-// Phase stagger of the large-n kernels (stagger_wait): the second CTA of
-// every SM waits kStaggerNs[N] at entry when the launch has several waves
-// (nbatches >= 4 x resident).  SEM_AX_STAGGER=ns[,lo,hi] overrides (tuning).
+// Phase stagger of co-resident CTAs (stagger_wait): the k-th resident CTA
+// of every SM waits (k - 1) x kStaggerNs[N] at entry when the launch has at
+// least 6 waves.  SEM_AX_STAGGER=ns[,lo,hi] overrides (tuning).
 // Scanned at E = 4096 with the defaults of kDefaultVariant (tools/
 // gpu_stagger.sh, profiles/r02_ax_stagger.txt; 1965 MHz): n = 12 73.0 ->
 // 72.2 us, 13 97.9 -> 94.6, 14 132.0 -> 129.4, 15 163.3 -> 155.4, 16 180.6 ->
-// 165.8; n = 11 (the only other two-per-SM default) flat, so 0.  The optimum
-// is a fraction of an element's time (~0.6-0.9) and sharp: the values sit
-// in the middle of each n's gain band.
-constexpr int kStaggerNs[17] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 3000, 5500, 4000, 10000, 11500};
+// 165.8 (two CTAs per SM); n = 10 (three per SM) 40.21 -> 40.04; n = 7, 9,
+// 11 flat, so 0.  The optimum is a fraction of an element's time (~0.3-0.9)
+// and sharp: the values sit in the middle of each n's gain band.
+constexpr int kStaggerNs[17] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1300, 0, 3000, 5500, 4000, 10000, 11500};
 template <int N>
 static void stagger_cfg(int minb, int64_t nbatches, int& ns, int& lo, int& hi)
 {
     static const char* env = getenv("SEM_AX_STAGGER");
     ns = 0;
     lo = sm_count();
-    hi = 2 * sm_count();
+    hi = minb * sm_count();
     if (env) {
+        hi = 2 * sm_count();
         sscanf(env, "%d,%d,%d", &ns, &lo, &hi);
         return;
     }
-    if (minb == 2 && nbatches >= 4 * (int64_t)minb * sm_count()) ns = kStaggerNs[N];
+    if (minb >= 2 && nbatches >= 6 * (int64_t)minb * sm_count()) ns = kStaggerNs[N];
 }
 
 template <int N, int SLOTS, int MINB, bool PERSIST, int PD = 1, int L2PF = 0, int GMODE = 0,

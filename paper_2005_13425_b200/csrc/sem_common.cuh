@@ -60,10 +60,12 @@ __device__ __forceinline__ void griddep_launch()
 // streams its metric (S4) while the other is in its shared-memory
 // contractions, and every later CTA inherits its slot's offset, so HBM
 // demand is spread over the element instead of arriving in per-wave bursts.
+// CTA b in [lo, hi) waits ns x (b / lo): with lo = the SM count, the k-th
+// resident CTA of an SM waits (k - 1) ns (hi = 2 lo: the second CTA only).
 __device__ __forceinline__ void stagger_wait(int ns, int lo, int hi)
 {
     if (ns <= 0 || (int)blockIdx.x < lo || (int)blockIdx.x >= hi) return;
-    const long long cycles = (long long)ns * 1965 / 1000;
+    const long long cycles = (long long)ns * ((int)blockIdx.x / lo) * 1965 / 1000;
     const long long t0 = clock64();
     do {
         __nanosleep(256);
