@@ -63,13 +63,17 @@ __device__ __forceinline__ void reduce_publish_and_finish(const double (&vals)[N
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int q = 0; q < NR; ++q) rs->partials[q][blockIdx.x] = tot[q];
-        __threadfence();
-        const unsigned prev = atomicAdd(&rs->counter, 1u);
+        // acq_rel arrival: releases this block's partials (thread 0 wrote
+        // them) and, in the last block, acquires every earlier block's; the
+        // barrier below then orders the other threads' loads after it (the
+        // semaphore pattern) -- no separate SC fences
+        unsigned prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                     : "=r"(prev) : "l"(&rs->counter) : "memory");
         am_last = (prev == gridDim.x - 1);
     }
     __syncthreads();
     if (!am_last) return;
-    __threadfence();
     double fin_tot[NR];
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
