@@ -293,10 +293,12 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     SEM_TRACE_ENTRY(st);
     griddep_wait();
     SEM_TRACE_WAITED(st);
-    // both state fields in one round trip (loaded before the stop branch)
+    // both state fields in one round trip; on the default path (alpha from
+    // the settle launch) the stop flag is first tested after the first row's
+    // loads are issued, so the state round trip overlaps them
     const int st_stop = st->stop;
     const double st_alpha = st->alpha;
-    if (st_stop) return;
+    if (st_stop && gathered != nullptr) return;
     double alpha;
     if (DIST && gathered != nullptr) {
         // multi-GPU phase-1 finish folded in: every CTA combines the ranks'
@@ -342,6 +344,7 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         // following the sum's additions
         load_row_rw<N>(r + base, rv);
         dssum_row<N>(w, rw, bx, DIST ? bot : nullptr, DIST ? top : nullptr, v);
+        if (st_stop) break;  // uniform: queued after a stop, nothing is written
 #pragma unroll
         for (int i = 0; i < N; ++i) {
             rv[i] = add_rn(rv[i], mul_rn(nalpha, mul_rn(v[i], row_mask<N>(rw, i))));
@@ -349,6 +352,7 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         }
         store_row<N>(r + base, rv);
     }
+    if (st_stop) return;
     if (!DIST) SEM_TRACE_EXIT(st, 2);
     griddep_launch();
     const double vals[1] = {acc};
@@ -613,8 +617,11 @@ cg_settle_kernel(const double* __restrict__ partials, int count, sem_cg_state* s
     griddep_wait();
     SEM_TRACE_WAITED(st);
     griddep_launch();
-    if (st->stop) return;
+    // the stop flag and the partials in one round trip (after a stop the
+    // partials are stale and unused)
+    const int stop = st->stop;
     const double tot = settle_sum<kSettleThreads>(partials, count);
+    if (stop) return;
     SEM_TRACE_EXIT(st, 1);
     if (threadIdx.x != 0) return;
     if (PH == kPhaseLocal) st->local_sum = (accumulate ? st->local_sum : 0.0) + tot;
