@@ -143,17 +143,25 @@ __device__ __forceinline__ void fin_init(sem_cg_state* st, double rtz)
 // pap_s: <p, A p> as the fused kernels accumulate it, scaled by
 // 2^(2k), k = pap_scale_exp(rtz) (sem_common.cuh): alpha = (rtz 2^(2k)) / pap_s
 // is the unscaled rtz / pap bit for bit in the normal range
-__device__ __forceinline__ void fin_pap(sem_cg_state* st, double pap_s)
+// rtz, it0: st->rtz, st->it as the calling kernel loaded them at entry (no
+// kernel changes them in between), so the finishing thread pays no further
+// state round trip after its sum
+__device__ __forceinline__ void fin_pap_v(sem_cg_state* st, double pap_s, double rtz, int it0)
 {
-    const int k = pap_scale_exp(st->rtz);
+    const int k = pap_scale_exp(rtz);
     st->pap = ldexp(pap_s, -2 * k);  // reported value (may underflow)
     st->x_pending = 0;  // the Ax prologues of this iteration applied it
     if (pap_s <= 0.0) {  // cg.py:164-169 breakdown
         st->stop = 2;
-        st->breakdown_it = st->it + 1;
+        st->breakdown_it = it0 + 1;
     } else {
-        st->alpha = ldexp(st->rtz, 2 * k) / pap_s;
+        st->alpha = ldexp(rtz, 2 * k) / pap_s;
     }
+}
+
+__device__ __forceinline__ void fin_pap(sem_cg_state* st, double pap_s)
+{
+    fin_pap_v(st, pap_s, st->rtz, st->it);
 }
 
 __device__ __forceinline__ void fin_rr(sem_cg_state* st, double rtr, double* history)
@@ -619,12 +627,14 @@ cg_settle_kernel(const double* __restrict__ partials, int count, sem_cg_state* s
     griddep_launch();
     // the stop flag and the partials in one round trip (after a stop the
     // partials are stale and unused)
-    const int stop = st->stop;
+    const int stop = st->stop, st_it = st->it;
+    const double st_rtz = st->rtz;
     const double tot = settle_sum<kSettleThreads>(partials, count);
     if (stop) return;
     SEM_TRACE_EXIT(st, 1);
     if (threadIdx.x != 0) return;
     if (PH == kPhaseLocal) st->local_sum = (accumulate ? st->local_sum : 0.0) + tot;
+    else if (PH == kPhasePap) fin_pap_v(st, tot, st_rtz, st_it);
     else fin_phase(st, PH, tot, history);
 }
 
