@@ -164,17 +164,32 @@ __device__ __forceinline__ void fin_pap(sem_cg_state* st, double pap_s)
     fin_pap_v(st, pap_s, st->rtz, st->it);
 }
 
-__device__ __forceinline__ void fin_rr(sem_cg_state* st, double rtr, double* history)
+// the state fields fin_rr reads, loaded ahead (reduce_publish_and_finish_pre)
+struct RrCtx {
+    int it0;
+    double rtz0, tol;
+};
+__device__ __forceinline__ RrCtx rr_ctx(const sem_cg_state* st)
 {
-    const int it = st->it + 1;
+    return RrCtx{st->it, st->rtz, st->tolerance};
+}
+
+__device__ __forceinline__ void fin_rr_v(sem_cg_state* st, double rtr, double* history, const RrCtx& c)
+{
+    const int it = c.it0 + 1;
     const double rnorm = sqrt(rtr);
     history[it - 1] = rnorm;
     st->iterations_run = it;
-    st->rtz_old = st->rtz;
+    st->rtz_old = c.rtz0;
     st->rtz = rtr;  // equals <r,r>_c at the top of the next iteration
     st->it = it;
     st->x_pending = 1;  // x += alpha p of this iteration: next Ax prologue / finalize
-    if (st->tolerance > 0.0 && rnorm < st->tolerance) st->stop = 3;
+    if (c.tol > 0.0 && rnorm < c.tol) st->stop = 3;
+}
+
+__device__ __forceinline__ void fin_rr(sem_cg_state* st, double rtr, double* history)
+{
+    fin_rr_v(st, rtr, history, rr_ctx(st));
 }
 
 __device__ __forceinline__ void fin_phase(sem_cg_state* st, int phase, double total,
@@ -368,10 +383,14 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
         reduce_publish_only<1, RT>(vals, rs);
         return;
     }
-    reduce_publish_and_finish<1, RT>(vals, rs, [&](const double (&t)[1]) {
-        if (DIST) st->local_sum = t[0];
-        else fin_rr(st, t[0], history);
-    });
+    // the last block's thread 0 loads the state fields fin_rr needs together
+    // with the partials (one round trip before the state is final)
+    reduce_publish_and_finish_pre<1, RT>(
+        vals, rs, [&] { return DIST ? RrCtx{} : rr_ctx(st); },
+        [&](const double (&t)[1], const RrCtx& c) {
+            if (DIST) st->local_sum = t[0];
+            else fin_rr_v(st, t[0], history, c);
+        });
 }
 
 // Element-granular form of the same iteration tail ("cube" update): each

@@ -49,11 +49,13 @@ __device__ __forceinline__ double block_sum(double v, double* sh /* >= THREADS/3
 }
 
 // Publish NR block partials; the last block to arrive combines them in
-// block order and calls fin(totals) from thread 0.  Returns true in the
-// finishing block.
-template <int NR, int THREADS, typename Fin>
-__device__ __forceinline__ void reduce_publish_and_finish(const double (&vals)[NR],
-                                                          ReduceScratch* rs, Fin fin)
+// block order and calls fin(totals, ctx) from thread 0, where ctx = pre()
+// was evaluated by that thread BEFORE the partials are loaded (pre issues the
+// loads fin needs -- e.g. state fields -- so they share the partials' round
+// trip instead of following the sum).
+template <int NR, int THREADS, typename Pre, typename Fin>
+__device__ __forceinline__ void reduce_publish_and_finish_pre(const double (&vals)[NR],
+                                                              ReduceScratch* rs, Pre pre, Fin fin)
 {
     __shared__ double sh[THREADS / 32];
     __shared__ bool am_last;
@@ -74,6 +76,8 @@ __device__ __forceinline__ void reduce_publish_and_finish(const double (&vals)[N
     }
     __syncthreads();
     if (!am_last) return;
+    decltype(pre()) ctx{};
+    if (threadIdx.x == 0) ctx = pre();
     double fin_tot[NR];
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
@@ -84,8 +88,17 @@ __device__ __forceinline__ void reduce_publish_and_finish(const double (&vals)[N
     }
     if (threadIdx.x == 0) {
         rs->counter = 0u;
-        fin(fin_tot);
+        fin(fin_tot, ctx);
     }
+}
+
+// The same without a prefetch: fin(totals) from thread 0 of the last block.
+template <int NR, int THREADS, typename Fin>
+__device__ __forceinline__ void reduce_publish_and_finish(const double (&vals)[NR],
+                                                          ReduceScratch* rs, Fin fin)
+{
+    reduce_publish_and_finish_pre<NR, THREADS>(
+        vals, rs, [] { return 0; }, [&](const double (&t)[NR], int) { fin(t); });
 }
 
 // Deferred form: publish this block's NR totals only (no fence, no arrival
