@@ -316,6 +316,9 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     SEM_TRACE_ENTRY(st);
     griddep_wait();
     SEM_TRACE_WAITED(st);
+#ifdef SEM_UPD_EARLY_TRIGGER
+    griddep_launch();  // tuning probe: the next Ax may take freed SM slots during the row loop
+#endif
     // both state fields in one round trip; on the default path (alpha from
     // the settle launch) the stop flag is first tested after the first row's
     // loads are issued, so the state round trip overlaps them
@@ -377,7 +380,9 @@ cg_update2_kernel(const double* __restrict__ w, double* __restrict__ r, int64_t 
     }
     if (st_stop) return;
     if (!DIST) SEM_TRACE_EXIT(st, 2);
+#ifndef SEM_UPD_EARLY_TRIGGER
     griddep_launch();
+#endif
     const double vals[1] = {acc};
     if (deferred) {  // single GPU: cg_settle_kernel finishes <r, r>
         reduce_publish_only<1, RT>(vals, rs);
